@@ -1,0 +1,228 @@
+"""Convolution engines over prime fields and the poly_mul dispatcher (GPU).
+
+Call-compatible with the reference's engine functions
+(/root/reference/pkg/src/modconv/convolve.py): ConvRequest, ENGINES,
+circ_conv_fft (:143-157), lin_conv_fft_pad (:160-169), conv_tft (:230-253)
+and poly_mul (:264-296), plus a batched tensor API (conv_batch) that is the
+hot path proper: [B, z1] x [B, z2] -> [B, n] in one kernel launch.
+
+Engines run in libmodconv_b200 (mc_conv_fft_pad / mc_conv_tft /
+mc_circ_conv).  `threads` is accepted and ignored (the GPU does not use host
+workers; results are schedule-independent like the reference's).  The
+quadratic "definition" engine is a CPU oracle in the reference; here it is
+served by the GPU fft_pad kernel (bit-identical output, no counters touched,
+exactly as lin_conv_def touches none).  "split" (Eq. 13) is not on the
+north-star path and raises.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field as dc_field
+
+import torch
+
+from . import _native, _tensors
+from .field import FieldMismatchError, as_field, check_transform_size
+from .poly import DensePoly
+from .transform import OpCounters, full_count, itft_count, tft_count
+
+ENGINES = ("definition", "fft_pad", "tft", "split", "auto")
+
+
+@dataclass
+class ConvRequest:
+    """How to run a convolution (convolve.py:33-47)."""
+
+    field: object
+    engine: str = "auto"
+    threads: int = 1
+    counters: OpCounters | None = None
+    planner: object = dc_field(default=None, repr=False)
+
+    def __post_init__(self) -> None:
+        if self.engine not in ENGINES:
+            raise ValueError(f"unknown engine {self.engine!r}; choose from {ENGINES}")
+        if self.threads < 1:
+            raise ValueError("threads must be >= 1")
+
+
+def _next_pow2(n: int) -> int:
+    return 1 << (n - 1).bit_length() if n > 1 else 1
+
+
+def count_engine(engine: str, z1: int, z2: int, counters: OpCounters | None, batch: int = 1):
+    """Reference OpCounters for one engine call (per product x batch)."""
+    if counters is None:
+        return
+    n = z1 + z2 - 1
+    L = _next_pow2(n)
+    if engine == "fft_pad":
+        counters.butterflies += 3 * full_count(L) * batch
+        counters.pointwise_muls += L * batch
+    elif engine == "tft":
+        bf = tft_count(L, z1, n) + tft_count(L, z2, n) + itft_count(L, n)
+        counters.butterflies += bf * batch
+        counters.pointwise_muls += n * batch
+
+
+# ------------------------------------------------------------------ batched API
+def _as_batch(x, name: str) -> torch.Tensor:
+    if not isinstance(x, torch.Tensor):
+        raise ValueError(f"{name} must be a torch tensor")
+    if x.dim() == 1:
+        x = x.unsqueeze(0)
+    if x.dim() != 2:
+        raise ValueError(f"{name} must be [batch, length]")
+    return _tensors.as_words(x)
+
+
+def conv_batch(a: torch.Tensor, b: torch.Tensor, field, engine: str = "tft",
+               out: torch.Tensor | None = None, counters: OpCounters | None = None,
+               stream=None) -> torch.Tensor:
+    """Row-wise linear convolution mod p of a [B, z1] and b [B, z2] -> [B, n].
+
+    Tensors hold canonical residues as int32 (or uint32).  CUDA inputs are
+    used in place (rows may be strided: any row stride >= row length);
+    CPU inputs are copied to the current device inside the call and the
+    result is copied back (the host-buffer path: H2D, kernel, D2H).
+    engine: "tft" (truncated transforms, convolve.py:230-253) or "fft_pad"
+    (zero-padded full transforms, convolve.py:160-169).
+    """
+    if engine not in ("tft", "fft_pad"):
+        raise ValueError(f"batched engine must be 'tft' or 'fft_pad', got {engine!r}")
+    fp = as_field(field)
+    a = _as_batch(a, "a")
+    b = _as_batch(b, "b")
+    if a.shape[0] != b.shape[0]:
+        raise ValueError(f"batch mismatch: {a.shape[0]} vs {b.shape[0]}")
+    B, z1 = a.shape
+    z2 = b.shape[1]
+    if z1 < 1 or z2 < 1:
+        raise ValueError("inputs must be nonempty")
+    n = z1 + z2 - 1
+    check_transform_size(fp, (_next_pow2(n)).bit_length() - 1)
+    dev = _tensors.require_cuda()
+    host = a.device.type == "cpu"
+    if host != (b.device.type == "cpu"):
+        raise ValueError("a and b must be on the same device")
+    if host:
+        a_d = a.to(dev, non_blocking=True)
+        b_d = b.to(dev, non_blocking=True)
+    else:
+        a_d, b_d = a, b
+    if a_d.stride(1) != 1 or b_d.stride(1) != 1:
+        a_d, b_d = a_d.contiguous(), b_d.contiguous()
+    if out is not None and not host:
+        c_d = _tensors.as_words(out)
+        if c_d.shape != (B, n) or c_d.stride(1) != 1:
+            raise ValueError(f"out must be [B, {n}] with unit column stride")
+    else:
+        c_d = torch.empty((B, n), dtype=torch.int32, device=dev)
+    fn = _native.lib().mc_conv_tft if engine == "tft" else _native.lib().mc_conv_fft_pad
+    _native.check(fn(_tensors.ptr(a_d), a_d.stride(0), z1, _tensors.ptr(b_d), b_d.stride(0), z2,
+                     _tensors.ptr(c_d), c_d.stride(0), B, fp.p, _tensors.stream_handle(stream)))
+    count_engine(engine, z1, z2, counters, B)
+    if host:
+        if out is not None:
+            out.copy_(c_d, non_blocking=True)
+            return out
+        return c_d.to("cpu")
+    return c_d
+
+
+# ------------------------------------------------------------------ list API
+def _run_lists(engine: str, u, v, req: ConvRequest) -> list[int]:
+    fp = as_field(req.field)
+    dev = _tensors.require_cuda()
+    a = _tensors.list_to_device(u, fp.p, dev).unsqueeze(0)
+    b = _tensors.list_to_device(v, fp.p, dev).unsqueeze(0)
+    c = conv_batch(a, b, fp, engine=engine)
+    return _tensors.device_to_list(c[0])
+
+
+def circ_conv_fft(u, v, req: ConvRequest) -> list[int]:
+    """Circular convolution of two power-of-two length vectors
+    (convolve.py:143-157)."""
+    n = len(u)
+    if n == 0 or len(v) != n:
+        raise ValueError(f"need equal nonempty lengths, got {len(u)} and {len(v)}")
+    if n & (n - 1):
+        raise ValueError(f"length must be a power of two: {n}")
+    fp = as_field(req.field)
+    check_transform_size(fp, n.bit_length() - 1)
+    dev = _tensors.require_cuda()
+    a = _tensors.list_to_device(u, fp.p, dev)
+    b = _tensors.list_to_device(v, fp.p, dev)
+    c = torch.empty_like(a)
+    _native.check(_native.lib().mc_circ_conv(_tensors.ptr(a), _tensors.ptr(b), _tensors.ptr(c),
+                                             n.bit_length() - 1, 1, fp.p,
+                                             _tensors.stream_handle()))
+    if req.counters is not None:
+        req.counters.butterflies += 3 * full_count(n)
+        req.counters.pointwise_muls += n
+    return _tensors.device_to_list(c)
+
+
+def lin_conv_fft_pad(u, v, req: ConvRequest) -> list[int]:
+    """Linear convolution by zero-padding to a power of two
+    (convolve.py:160-169).  Output not normalized."""
+    if len(u) == 0 or len(v) == 0:
+        raise ValueError("inputs must be nonempty")
+    out = _run_lists("fft_pad", u, v, req)
+    count_engine("fft_pad", len(u), len(v), req.counters)
+    return out
+
+
+def conv_tft(g, h, req: ConvRequest) -> list[int]:
+    """Linear convolution via truncated transforms (convolve.py:230-253)."""
+    if len(g) == 0 or len(h) == 0:
+        raise ValueError("inputs must be nonempty")
+    out = _run_lists("tft", g, h, req)
+    count_engine("tft", len(g), len(h), req.counters)
+    return out
+
+
+def _resolve_engine(a_len: int, b_len: int, req: ConvRequest) -> str:
+    if req.engine != "auto":
+        return req.engine
+    if req.planner is None:
+        raise ValueError("engine 'auto' requires a ConvRequest.planner plan session")
+    return req.planner.resolve_engine(req.field, a_len, b_len, req.threads)
+
+
+def poly_mul(a, b, req: ConvRequest) -> DensePoly:
+    """Multiply polynomials with the requested engine (convolve.py:264-296).
+
+    Zero inputs short-circuit without touching any transform or counter;
+    inputs are normalized first; the result is normalized.  Accepts this
+    package's DensePoly or any object with .field.p and .coeffs (e.g. the
+    reference's own DensePoly).
+    """
+    if a.field.p != b.field.p:
+        raise FieldMismatchError(f"mixed moduli {a.field.p} and {b.field.p}")
+    if a.field.p != req.field.p:
+        raise FieldMismatchError(f"request field {req.field.p} does not match operands {a.field.p}")
+    fp = as_field(req.field)
+    if not any(a.coeffs) or not any(b.coeffs):
+        return DensePoly.zero(fp)
+    u = _trim(a.coeffs)
+    v = _trim(b.coeffs)
+    engine = _resolve_engine(len(u), len(v), req)
+    if engine == "definition":
+        out = _run_lists("fft_pad", u, v, req)
+    elif engine == "fft_pad":
+        out = lin_conv_fft_pad(u, v, req)
+    elif engine == "tft":
+        out = conv_tft(u, v, req)
+    elif engine == "split":
+        raise ValueError("engine 'split' (convolve.py:193-227) is not provided by the GPU path")
+    else:
+        raise ValueError(f"unknown engine {engine!r}")
+    return DensePoly(fp, tuple(out)).normalize()
+
+
+def _trim(coeffs) -> list[int]:
+    c = list(coeffs)
+    while c and not c[-1]:
+        c.pop()
+    return c

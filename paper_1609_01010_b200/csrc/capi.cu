@@ -1,0 +1,248 @@
+// C ABI entry points (include/modconv_b200.h): argument checking, table
+// lookup, kernel selection.  No torch types cross this boundary.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "conv_small.cuh"
+#include "fourstep.cuh"
+#include "runtime.h"
+
+namespace mc {
+
+cudaError_t launch_conv_small_k4(const ConvSmallParams &, int, cudaStream_t);
+cudaError_t launch_conv_small_k5(const ConvSmallParams &, int, cudaStream_t);
+cudaError_t launch_conv_small_k6(const ConvSmallParams &, int, cudaStream_t);
+cudaError_t launch_conv_small_k7(const ConvSmallParams &, int, cudaStream_t);
+cudaError_t launch_conv_small_k8(const ConvSmallParams &, int, cudaStream_t);
+cudaError_t launch_conv_small_k9(const ConvSmallParams &, int, cudaStream_t);
+cudaError_t launch_conv_small_k10(const ConvSmallParams &, int, cudaStream_t);
+cudaError_t launch_conv_small_k11(const ConvSmallParams &, int, cudaStream_t);
+cudaError_t launch_conv_small_k12(const ConvSmallParams &, int, cudaStream_t);
+cudaError_t launch_conv_small_k13(const ConvSmallParams &, int, cudaStream_t);
+
+static const int kSmallMaxK = 13;
+
+// ---------------------------------------------------------------- tiny sizes
+// L <= 8: one thread per product, direct convolution with 64-bit
+// accumulation (exact; lin_conv_def semantics, convolve.py:71-87).
+__global__ void conv_tiny_kernel(const u32 *a, long long lda, int z1, const u32 *b,
+                                 long long ldb, int z2, u32 *c, long long ldc,
+                                 long long batch, u32 p, int wrap_L) {
+    long long r = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= batch) return;
+    const u32 *ar = a + r * lda;
+    const u32 *br = b + r * ldb;
+    u32 *cr = c + r * ldc;
+    const int n = wrap_L ? wrap_L : z1 + z2 - 1;
+    for (int k = 0; k < n; ++k) {
+        unsigned long long acc = 0;
+        for (int i = 0; i < z1; ++i) {
+            for (int j = 0; j < z2; ++j) {
+                int d = i + j;
+                if (wrap_L) d &= wrap_L - 1;
+                if (d == k) acc = (acc + (unsigned long long)ar[i] * br[j]) % p;
+            }
+        }
+        cr[k] = (u32)acc;
+    }
+}
+
+static int ceil_log2(long long n) {
+    int k = 0;
+    while ((1ll << k) < n) ++k;
+    return k;
+}
+
+static ConvSmallParams make_params(const FieldTables *T, const u32 *a, long long lda, int z1,
+                                   const u32 *b, long long ldb, int z2, u32 *c, long long ldc,
+                                   int n, long long batch) {
+    ConvSmallParams P;
+    memset(&P, 0, sizeof(P));
+    P.a = a;
+    P.b = b;
+    P.c = c;
+    P.lda = lda;
+    P.ldb = ldb;
+    P.ldc = ldc;
+    P.z1 = z1;
+    P.z2 = z2;
+    P.n = n;
+    P.batch = batch;
+    P.p = T->p;
+    P.pinv = T->pinv;
+    P.linv_mont = T->linv_mont;
+    P.tf = T->tf;
+    P.ti = T->ti;
+    const int K = T->log2L;
+    if (K >= 4) {
+        const u64 G = 1ull << (K - 4);
+        for (int l = 1; l <= 4; ++l) {
+            u64 m = (G << l) % T->p;
+            u64 h = (G << (l - 1)) % T->p;
+            P.mlev[l] = shoup((u32)m, T->p);
+            P.hinv[l] = shoup(inv_mod((u32)h, T->p), T->p);
+        }
+    }
+    return P;
+}
+
+static cudaError_t launch_small(int K, const ConvSmallParams &P, int nt, cudaStream_t st) {
+    switch (K) {
+        case 4: return launch_conv_small_k4(P, nt, st);
+        case 5: return launch_conv_small_k5(P, nt, st);
+        case 6: return launch_conv_small_k6(P, nt, st);
+        case 7: return launch_conv_small_k7(P, nt, st);
+        case 8: return launch_conv_small_k8(P, nt, st);
+        case 9: return launch_conv_small_k9(P, nt, st);
+        case 10: return launch_conv_small_k10(P, nt, st);
+        case 11: return launch_conv_small_k11(P, nt, st);
+        case 12: return launch_conv_small_k12(P, nt, st);
+        case 13: return launch_conv_small_k13(P, nt, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// engine 0 = fft_pad, 1 = tft; wrap != 0 => circular convolution of length L
+static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, const u32 *b,
+                               long long ldb, int z2, u32 *c, long long ldc, long long batch,
+                               u32 p, cudaStream_t st, int circ_log2L = -1) {
+    if (z1 < 1 || z2 < 1) return fail(MC_EINVAL, "inputs must be nonempty");
+    if (batch < 0) return fail(MC_EINVAL, "negative batch");
+    if (lda < z1 || ldb < z2) return fail(MC_EINVAL, "leading dimension smaller than row length");
+    const bool circ = circ_log2L >= 0;
+    const int n = circ ? (1 << circ_log2L) : z1 + z2 - 1;
+    if (ldc < n) return fail(MC_EINVAL, "output leading dimension smaller than product length");
+    const int K = circ ? circ_log2L : ceil_log2(n);
+    const FieldTables *T;
+    mc_status s = get_tables(p, K, &T);
+    if (s != MC_OK) return s;
+    if (batch == 0) return MC_OK;
+    if (!a || !b || !c) return fail(MC_EINVAL, "null pointer");
+    if (K <= 3) {
+        const int thr = 128;
+        conv_tiny_kernel<<<(unsigned)((batch + thr - 1) / thr), thr, 0, st>>>(
+            a, lda, z1, b, ldb, z2, c, ldc, batch, p, circ ? (1 << K) : 0);
+        note_launches(1);
+        MC_CUDA_CHECK(cudaGetLastError());
+        return MC_OK;
+    }
+    if (K <= kSmallMaxK) {
+        ConvSmallParams P = make_params(T, a, lda, z1, b, ldb, z2, c, ldc, n, batch);
+        int nt = 16;
+        if (engine == 1 && !circ) {
+            const int G = 1 << (K - 4);
+            nt = (n + G - 1) / G;
+        }
+        if (batch > 0x7fffffffll * SmallCfg<4>::PPC)
+            return fail(MC_EINVAL, "batch too large for one launch");
+        cudaError_t e = launch_small(K, P, nt, st);
+        note_launches(1);
+        if (e != cudaSuccess) return cuda_fail(e, "conv_small launch");
+        return MC_OK;
+    }
+    return fourstep_conv(engine, a, lda, z1, b, ldb, z2, c, ldc, batch, p, st, circ_log2L);
+}
+
+}  // namespace mc
+
+using namespace mc;
+
+extern "C" {
+
+mc_status mc_conv_fft_pad(const uint32_t *a, int64_t lda, int32_t z1, const uint32_t *b,
+                          int64_t ldb, int32_t z2, uint32_t *c, int64_t ldc, int64_t batch,
+                          uint32_t p, void *stream) {
+    return conv_dispatch(0, a, lda, z1, b, ldb, z2, c, ldc, batch, p, (cudaStream_t)stream);
+}
+
+mc_status mc_conv_tft(const uint32_t *a, int64_t lda, int32_t z1, const uint32_t *b,
+                      int64_t ldb, int32_t z2, uint32_t *c, int64_t ldc, int64_t batch,
+                      uint32_t p, void *stream) {
+    return conv_dispatch(1, a, lda, z1, b, ldb, z2, c, ldc, batch, p, (cudaStream_t)stream);
+}
+
+mc_status mc_circ_conv(const uint32_t *u, const uint32_t *v, uint32_t *w, int32_t log2L,
+                       int64_t batch, uint32_t p, void *stream) {
+    if (log2L < 0 || log2L > 30) return fail(MC_EINVAL, "bad transform size");
+    const int64_t L = 1ll << log2L;
+    return conv_dispatch(0, u, L, (int)L, v, L, (int)L, w, L, batch, p, (cudaStream_t)stream,
+                         log2L);
+}
+
+// ---------------------------------------------------------------- host-buffer call
+struct HostBufs {
+    void *d = nullptr;
+    size_t bytes = 0;
+    int dev = -1;
+    ~HostBufs() {
+        if (d) cudaFree(d);
+    }
+};
+
+mc_status mc_conv_host(int engine, const uint32_t *a, int64_t lda, int32_t z1,
+                       const uint32_t *b, int64_t ldb, int32_t z2, uint32_t *c, int64_t ldc,
+                       int64_t batch, uint32_t p) {
+    static thread_local HostBufs buf;
+    if (engine != 0 && engine != 1) return fail(MC_EINVAL, "engine must be 0 (fft_pad) or 1 (tft)");
+    if (z1 < 1 || z2 < 1) return fail(MC_EINVAL, "inputs must be nonempty");
+    const int64_t n = (int64_t)z1 + z2 - 1;
+    if (lda < z1 || ldb < z2 || ldc < n) return fail(MC_EINVAL, "bad leading dimension");
+    if (batch <= 0) return batch == 0 ? MC_OK : fail(MC_EINVAL, "negative batch");
+    const size_t need = 4ull * batch * (z1 + z2 + n);
+    int dev = current_device();
+    if (buf.bytes < need || buf.dev != dev) {
+        if (buf.d) cudaFree(buf.d);
+        buf.d = nullptr;
+        buf.bytes = 0;
+        MC_CUDA_CHECK(cudaMalloc(&buf.d, need));
+        buf.bytes = need;
+        buf.dev = dev;
+    }
+    uint32_t *da = (uint32_t *)buf.d, *db = da + batch * z1, *dc = db + batch * z2;
+    MC_CUDA_CHECK(cudaMemcpy2D(da, 4 * z1, a, 4 * lda, 4 * z1, batch, cudaMemcpyHostToDevice));
+    MC_CUDA_CHECK(cudaMemcpy2D(db, 4 * z2, b, 4 * ldb, 4 * z2, batch, cudaMemcpyHostToDevice));
+    mc_status s = conv_dispatch(engine, da, z1, z1, db, z2, z2, dc, n, batch, p, 0);
+    if (s != MC_OK) return s;
+    MC_CUDA_CHECK(cudaMemcpy2D(c, 4 * ldc, dc, 4 * n, 4 * n, batch, cudaMemcpyDeviceToHost));
+    return MC_OK;
+}
+
+// ---------------------------------------------------------------- generator
+__device__ __forceinline__ unsigned long long sm64(unsigned long long x) {
+    unsigned long long z = x + 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void gen_kernel(unsigned long long seed, unsigned long long sid,
+                           unsigned long long row0, long long rows, long long len,
+                           unsigned long long hi, uint32_t *out, long long ld) {
+    const long long r = blockIdx.y + (long long)blockIdx.z * gridDim.y;
+    if (r >= rows) return;
+    const unsigned long long key = sm64(sm64(sm64(seed) ^ sid) ^ (row0 + r));
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+         i += (long long)gridDim.x * blockDim.x) {
+        unsigned long long v = sm64(key + (unsigned long long)i);
+        out[r * ld + i] = (uint32_t)(((v >> 32) * hi) >> 32);
+    }
+}
+
+mc_status mc_gen_u32(uint64_t seed, uint64_t sid, uint64_t row0, int64_t rows, int64_t len,
+                     uint64_t hi, uint32_t *out, int64_t ld, void *stream) {
+    if (rows < 0 || len < 0 || ld < len || hi == 0 || hi > (1ull << 32))
+        return fail(MC_EINVAL, "bad generator arguments");
+    if (rows == 0 || len == 0) return MC_OK;
+    const int thr = 256;
+    long long bx = std::min<long long>((len + thr - 1) / thr, 64);
+    long long gy = std::min<long long>(rows, 65535);
+    long long gz = (rows + gy - 1) / gy;
+    gen_kernel<<<dim3((unsigned)bx, (unsigned)gy, (unsigned)gz), thr, 0, (cudaStream_t)stream>>>(
+        seed, sid, row0, rows, len, hi, out, ld);
+    note_launches(1);
+    MC_CUDA_CHECK(cudaGetLastError());
+    return MC_OK;
+}
+
+}  // extern "C"

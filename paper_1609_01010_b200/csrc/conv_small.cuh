@@ -1,0 +1,320 @@
+// Fused single-CTA convolution kernel for transform sizes 16 <= L <= 8192
+// (configs 1-3): forward transform of both operands, pointwise product with
+// L^-1 folded in, inverse transform, all in registers + shared memory, one
+// HBM read of each operand and one HBM write of the product.
+//
+// Replaces, per product row:
+//   fft_pad: convolve.py:160-169 -> :143-157 (moddft x3 + _pointwise)
+//   tft:     convolve.py:230-253 (tft x2 + _pointwise + itft + scale)
+//
+// Layout.  L = 2^K, G = L/16.  A product is owned by T = G threads, each
+// holding 16 "slots" per operand in registers.  Position bits are processed
+// in passes of <= 4 bits (radix-16 register passes): the top pass owns bits
+// [K-4, K) (thread t holds x = t + G*s), lower passes own 4-bit windows
+// [SB, SB+4) of lower bits.  Between passes the slots go through shared
+// memory under the XOR swizzle swz() that makes every pass's 32-lane access
+// hit 32 distinct banks.  Global loads/stores happen in the top-pass layout:
+// for each slot a warp touches 32 consecutive words (128 B).
+//
+// Transforms.  Forward = decimation in frequency (natural in, bit-reversed
+// out, the order of the reference TFT, transform.py:379-418) with direct
+// per-stage twiddles tf[h + j] = w_{2h}^j; inverse = decimation in time on
+// bit-reversed input with ti[h + j] = w_{2h}^-j (transform.py:150-164 run on
+// the bit-reversed spectrum).  No bit-reversal permutation is ever done.
+//
+// Truncation (tft engine, and zero padding in both engines).  The top pass
+// prunes butterflies exactly as the reference recursion does (known-zero
+// inputs: position offset within its block >= z; unneeded outputs: block
+// start >= n').  Truncation is "relaxed" to the G-block: n' = NT*G with
+// NT = ceil(n/G) in [9, 16]; G-blocks >= NT are skipped by every lower pass
+// and their spectral values are never formed.  The inverse runs the complete
+// inverse DIT on the NT active G-blocks (lower passes), then the
+// van der Hoeven inverse truncated recursion (transform.py:451-489) over the
+// top 4 levels with base case m == G, fully unrolled for the compile-time NT.
+// The product is exact either way (u_j = 0 for j >= n >= ... ), so the
+// output equals the reference's bit for bit; see tests/kernel_model.py for
+// the position-level model checked against the oracle.
+#pragma once
+#include "modarith.cuh"
+
+namespace mc {
+
+struct ConvSmallParams {
+    const u32 *a;
+    const u32 *b;
+    u32 *c;
+    long long lda, ldb, ldc;
+    int z1, z2, n;
+    long long batch;
+    u32 p, pinv;
+    Shoup linv_mont;   // L^-1 * 2^32 mod p
+    const uint2 *tf;   // forward stage twiddles
+    const uint2 *ti;   // inverse stage twiddles
+    Shoup mlev[5];     // [l] = (2^l * G) mod p, l = 1..4  (m of a top level)
+    Shoup hinv[5];     // [l] = (2^(l-1) * G)^-1 mod p    (1/h of a top level)
+};
+
+// 32-bank conflict-free swizzle for the three access patterns used here:
+// lanes -> position bits [0,5), [4,9), or [0,4) + {8}.  XOR touches only the
+// low 5 bits, so it is a permutation of every aligned 32-word row.
+__device__ __forceinline__ int swz(int x) { return x ^ (((x >> 5) & 15) | ((x >> 4) & 16)); }
+
+template <int SB>
+__device__ __forceinline__ int slot_pos(int t, int s) {
+    return ((t >> SB) << (SB + 4)) | (s << SB) | (t & ((1 << SB) - 1));
+}
+
+__device__ __forceinline__ uint2 ldtw(const uint2 *tab, int i) { return __ldg(tab + i); }
+
+// ---------------------------------------------------------------- top pass (forward)
+// Stages with half-size h = H*G, H = 8, 4, 2, 1 on slots (s, s+H).
+template <int K, int NT>
+__device__ __forceinline__ void fwd_top(u32 (&v)[16], int z, int t, const ConvSmallParams &P) {
+    constexpr int G = 1 << (K - 4);
+    const u32 p = P.p;
+#pragma unroll
+    for (int lv = 3; lv >= 0; --lv) {
+        const int H = 1 << lv;
+        const int h = H * G;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            if (s & H) continue;
+            const int sblk = s & ~(2 * H - 1);
+            if (sblk >= NT) continue;                 // whole block unneeded
+            const bool hi_needed = (sblk + H) < NT;
+            const int jel = t + G * (s & (2 * H - 1));  // offset within the 2h block
+            if (jel < z) {
+                if (jel + h < z) {
+                    if (hi_needed) {
+                        const uint2 w = ldtw(P.tf, h + jel);
+                        bfly_dif(v[s], v[s + H], w.x, w.y, p);
+                    } else {
+                        v[s] = add_mod(v[s], v[s + H], p);  // lo-only add (fold)
+                    }
+                } else if (hi_needed) {
+                    const uint2 w = ldtw(P.tf, h + jel);    // hi input is zero
+                    v[s + H] = mul_shoup(v[s], w.x, w.y, p);
+                }
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- lower passes
+template <int K, int LO, int HI, int SB>
+__device__ __forceinline__ void fwd_lower(u32 (&v)[16], int t, const ConvSmallParams &P) {
+    const u32 p = P.p;
+    const int tpos = slot_pos<SB>(t, 0);
+#pragma unroll
+    for (int b = HI - 1; b >= LO; --b) {
+        const int h = 1 << b;
+        const int sbit = b - SB;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            if ((s >> sbit) & 1) continue;
+            const int j = (tpos | (s << SB)) & (h - 1);
+            const uint2 w = ldtw(P.tf, h + j);
+            bfly_dif(v[s], v[s | (1 << sbit)], w.x, w.y, p);
+        }
+    }
+}
+
+template <int K, int LO, int HI, int SB>
+__device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallParams &P) {
+    const u32 p = P.p;
+    const int tpos = slot_pos<SB>(t, 0);
+#pragma unroll
+    for (int b = LO; b < HI; ++b) {
+        const int h = 1 << b;
+        const int sbit = b - SB;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            if ((s >> sbit) & 1) continue;
+            const int j = (tpos | (s << SB)) & (h - 1);
+            const uint2 w = ldtw(P.ti, h + j);
+            bfly_dit(v[s], v[s | (1 << sbit)], w.x, w.y, p);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- top pass (inverse)
+// transform.py:451-489 restricted to slot granularity.  M, N, OFF in slots;
+// level index LV = log2 M (m = M*G elements).
+template <int K, int M, int N, int OFF>
+struct ItftTop {
+    static __device__ __forceinline__ void run(u32 (&v)[16], int t, const ConvSmallParams &P) {
+        constexpr int G = 1 << (K - 4);
+        constexpr int H = M / 2;
+        constexpr int LV = (M == 16) ? 4 : (M == 8) ? 3 : (M == 4) ? 2 : 1;
+        const u32 p = P.p;
+        if constexpr (M == 1 || N == 0) {
+            return;
+        } else if constexpr (N <= H) {
+            // pre: time values of both halves folded into the first half
+#pragma unroll
+            for (int s = N; s < H; ++s) v[OFF + s] = add_mod(v[OFF + s], v[OFF + s + H], p);
+            ItftTop<K, H, N, OFF>::run(v, t, P);
+            // combine: m*u_i = 2*(h*(u_i + u_{i+h})) - m*u_{i+h}
+            const Shoup mm = P.mlev[LV];
+#pragma unroll
+            for (int s = 0; s < N; ++s) {
+                u32 a = v[OFF + s];
+                v[OFF + s] = sub_mod(add_mod(a, a, p), mul_shoup(v[OFF + s + H], mm, p), p);
+            }
+        } else {
+            ItftTop<K, H, H, OFF>::run(v, t, P);  // complete first half
+            const Shoup mm = P.mlev[LV];
+            const Shoup ih = P.hinv[LV];
+            constexpr int h = H * G;
+#pragma unroll
+            for (int s = N - H; s < H; ++s) {  // cross butterflies
+                u32 a = v[OFF + s], b = v[OFF + s + H];
+                const uint2 w = ldtw(P.tf, h + t + G * s);
+                u32 d = sub_mod(mul_shoup(a, ih, p), add_mod(b, b, p), p);
+                v[OFF + s + H] = mul_shoup(d, w.x, w.y, p);
+                v[OFF + s] = sub_mod(add_mod(a, a, p), mul_shoup(b, mm, p), p);
+            }
+            ItftTop<K, H, N - H, OFF + H>::run(v, t, P);
+#pragma unroll
+            for (int s = 0; s < N - H; ++s) {  // inverse DIT butterflies
+                const uint2 w = ldtw(P.ti, h + t + G * s);
+                bfly_dit(v[OFF + s], v[OFF + s + H], w.x, w.y, p);
+            }
+        }
+    }
+};
+
+// ---------------------------------------------------------------- exchange
+template <int SB>
+__device__ __forceinline__ void put(u32 *buf, const u32 (&v)[16], int t) {
+#pragma unroll
+    for (int s = 0; s < 16; ++s) buf[swz(slot_pos<SB>(t, s))] = v[s];
+}
+
+template <int SB>
+__device__ __forceinline__ void get(const u32 *buf, u32 (&v)[16], int t) {
+#pragma unroll
+    for (int s = 0; s < 16; ++s) v[s] = buf[swz(slot_pos<SB>(t, s))];
+}
+
+// Lower-pass plan for K: up to three passes (bits [8,KL), [4,8), [0,4) with
+// KL = K - 4), each with its slot window base SB.
+template <int K>
+struct Plan {
+    static constexpr int KL = K - 4;
+    static constexpr int NP = KL == 0 ? 0 : KL <= 4 ? 1 : KL <= 8 ? 2 : 3;
+    // pass i (0 = highest bits)
+    static constexpr int lo(int i) { return NP == 3 ? (i == 0 ? 8 : i == 1 ? 4 : 0)
+                                          : NP == 2 ? (i == 0 ? 4 : 0) : 0; }
+    static constexpr int hi(int i) { return NP == 3 ? (i == 0 ? KL : i == 1 ? 8 : 4)
+                                          : NP == 2 ? (i == 0 ? KL : 4) : KL; }
+    static constexpr int sb(int i) { return lo(i); }
+};
+
+template <int K, int I>
+__device__ __forceinline__ int gblock_of_pass(int t) {
+    return slot_pos<Plan<K>::sb(I)>(t, 0) >> (K - 4);
+}
+
+template <int K, int NT, int I>
+__device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[16], u32 (&vb)[16],
+                                                int t, const ConvSmallParams &P) {
+    if constexpr (I < Plan<K>::NP) {
+        constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
+        constexpr int SB = Plan<K>::sb(I);
+        __syncthreads();
+        put<SBprev>(bufA, va, t);
+        put<SBprev>(bufB, vb, t);
+        __syncthreads();
+        get<SB>(bufA, va, t);
+        get<SB>(bufB, vb, t);
+        if (NT >= 16 || gblock_of_pass<K, I>(t) < NT) {
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(va, t, P);
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(vb, t, P);
+        }
+        fwd_lower_chain<K, NT, I + 1>(bufA, bufB, va, vb, t, P);
+    }
+}
+
+// Inverse lower passes in reverse order (lowest bits first); on exit the
+// slots are in the top-pass layout.
+template <int K, int NT, int I>
+__device__ __forceinline__ void inv_lower_chain(u32 *buf, u32 (&v)[16], int t,
+                                                const ConvSmallParams &P) {
+    if constexpr (I >= 0) {
+        constexpr int SB = Plan<K>::sb(I);
+        constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
+        if (NT >= 16 || gblock_of_pass<K, I>(t) < NT)
+            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(v, t, P);
+        __syncthreads();
+        put<SB>(buf, v, t);
+        __syncthreads();
+        get<SBnext>(buf, v, t);
+        inv_lower_chain<K, NT, I - 1>(buf, v, t, P);
+    }
+}
+
+template <int K>
+struct SmallCfg {
+    static constexpr int L = 1 << K;
+    static constexpr int T = L / 16;
+    static constexpr int PPC = T >= 128 ? 1 : 128 / T;  // products per CTA
+    static constexpr int THREADS = T * PPC;
+    static constexpr int SMEM = PPC * 2 * L * 4;
+};
+
+template <int K, int NT>
+__global__ void __launch_bounds__(SmallCfg<K>::THREADS)
+conv_small_kernel(const ConvSmallParams P) {
+    using C = SmallCfg<K>;
+    constexpr int L = C::L, T = C::T;
+    extern __shared__ u32 smem[];
+    const int grp = threadIdx.x / T;
+    const int t = threadIdx.x % T;
+    const long long row = (long long)blockIdx.x * C::PPC + grp;
+    const bool valid = row < P.batch;
+    u32 *bufA = smem + grp * 2 * L;
+    u32 *bufB = bufA + L;
+
+    u32 va[16], vb[16];
+    const u32 *ga = P.a + (valid ? row : 0) * P.lda;
+    const u32 *gb = P.b + (valid ? row : 0) * P.ldb;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const int x = (s << (K - 4)) | t;
+        va[s] = (valid && x < P.z1) ? __ldcs(ga + x) : 0u;
+        vb[s] = (valid && x < P.z2) ? __ldcs(gb + x) : 0u;
+    }
+
+    fwd_top<K, NT>(va, P.z1, t, P);
+    fwd_top<K, NT>(vb, P.z2, t, P);
+    fwd_lower_chain<K, NT, 0>(bufA, bufB, va, vb, t, P);
+
+    // pointwise product in the last pass's layout, L^-1 folded in
+    {
+        constexpr int LAST = Plan<K>::NP - 1;
+        constexpr int SB = (Plan<K>::NP == 0) ? (K - 4) : Plan<K>::sb(LAST < 0 ? 0 : LAST);
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const int x = slot_pos<SB>(t, s);
+            if (NT >= 16 || (x >> (K - 4)) < NT)
+                va[s] = mul_shoup(mont_mul(va[s], vb[s], P.p, P.pinv), P.linv_mont, P.p);
+            else
+                va[s] = 0u;  // time values of the inactive tail: u_j = 0
+        }
+    }
+
+    inv_lower_chain<K, NT, Plan<K>::NP - 1>(bufA, va, t, P);
+    ItftTop<K, 16, NT, 0>::run(va, t, P);
+
+    if (valid) {
+        u32 *gc = P.c + row * P.ldc;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const int x = (s << (K - 4)) | t;
+            if (x < P.n) __stcs(gc + x, va[s]);
+        }
+    }
+}
+
+}  // namespace mc

@@ -1,0 +1,45 @@
+// Instantiations of the fused small-L convolution kernel for one K
+// (compiled once per K with -DMC_K=<K> so the 10 sizes build in parallel).
+#include "conv_small.cuh"
+#include "runtime.h"
+
+#ifndef MC_K
+#error "compile with -DMC_K=<log2 L>"
+#endif
+
+namespace mc {
+
+template <int NT>
+static cudaError_t launch_nt(const ConvSmallParams &P, cudaStream_t st) {
+    using C = SmallCfg<MC_K>;
+    auto kern = conv_small_kernel<MC_K, NT>;
+    static bool attr_done = false;  // benign race: idempotent attribute set
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             C::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    const long long grid = (P.batch + C::PPC - 1) / C::PPC;
+    kern<<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(P);
+    return cudaGetLastError();
+}
+
+#define MC_CAT2(a, b) a##b
+#define MC_CAT(a, b) MC_CAT2(a, b)
+
+cudaError_t MC_CAT(launch_conv_small_k, MC_K)(const ConvSmallParams &P, int nt, cudaStream_t st) {
+    switch (nt) {
+        case 9: return launch_nt<9>(P, st);
+        case 10: return launch_nt<10>(P, st);
+        case 11: return launch_nt<11>(P, st);
+        case 12: return launch_nt<12>(P, st);
+        case 13: return launch_nt<13>(P, st);
+        case 14: return launch_nt<14>(P, st);
+        case 15: return launch_nt<15>(P, st);
+        case 16: return launch_nt<16>(P, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace mc

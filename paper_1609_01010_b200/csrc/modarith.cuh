@@ -1,0 +1,81 @@
+// Word-size modular arithmetic on the sm_100a integer pipes.
+//
+// Residues are uint32 in [0, p), p < 2^31 (so 2p < 2^32 and every lazy sum
+// below fits in a word).  Fixed operands (twiddles, scale constants) use
+// Shoup's precomputed quotient: w' = floor(w * 2^32 / p), and
+//   q = umulhi(x, w');  r = x*w - q*p      in [0, 2p) for ANY x < 2^32,
+// i.e. IMAD.HI + IMUL + IMAD.  Variable x variable products (the pointwise
+// spectral product) use Montgomery REDC with R = 2^32.
+//
+// The reference performs the same arithmetic with Python ints and `%`
+// (transform.py:160-163 butterfly, convolve.py:123 pointwise); every helper
+// here returns the canonical residue, so results are bit-identical.
+#pragma once
+#include <cstdint>
+
+namespace mc {
+
+typedef uint32_t u32;
+typedef uint64_t u64;
+
+struct Shoup {
+    u32 w;   // multiplier in [0, p)
+    u32 wp;  // floor(w * 2^32 / p)
+};
+
+// [0, 2p) -> [0, p).  Unsigned min: if x < p then x - p wraps above x.
+__device__ __forceinline__ u32 red1(u32 x, u32 p) { return min(x, x - p); }
+
+__device__ __forceinline__ u32 add_mod(u32 a, u32 b, u32 p) {
+    u32 s = a + b;
+    return min(s, s - p);
+}
+
+__device__ __forceinline__ u32 sub_mod(u32 a, u32 b, u32 p) {
+    u32 d = a - b + p;
+    return min(d, d - p);
+}
+
+// x * w mod p in [0, 2p), any 32-bit x.
+__device__ __forceinline__ u32 mul_shoup_lazy(u32 x, u32 w, u32 wp, u32 p) {
+    u32 q = __umulhi(x, wp);
+    return x * w - q * p;
+}
+
+__device__ __forceinline__ u32 mul_shoup(u32 x, u32 w, u32 wp, u32 p) {
+    return red1(mul_shoup_lazy(x, w, wp, p), p);
+}
+
+__device__ __forceinline__ u32 mul_shoup(u32 x, Shoup s, u32 p) {
+    return mul_shoup(x, s.w, s.wp, p);
+}
+
+// Montgomery product a*b*2^-32 mod p, canonical.  pinv = p^-1 mod 2^32.
+// a*b - m*p is divisible by 2^32 with m = lo*pinv, and its quotient
+// hi - umulhi(m, p) lies in (-p, p).
+__device__ __forceinline__ u32 mont_mul(u32 a, u32 b, u32 p, u32 pinv) {
+    u32 lo = a * b;
+    u32 hi = __umulhi(a, b);
+    u32 m = lo * pinv;
+    u32 r = hi - __umulhi(m, p);
+    return min(r, r + p);
+}
+
+// Decimation-in-frequency butterfly (Gentleman-Sande):
+//   lo = a + b,  hi = (a - b) * w          (transform.py:390-393)
+__device__ __forceinline__ void bfly_dif(u32 &a, u32 &b, u32 w, u32 wp, u32 p) {
+    u32 s = add_mod(a, b, p);
+    b = mul_shoup(a - b + p, w, wp, p);
+    a = s;
+}
+
+// Decimation-in-time butterfly (Cooley-Tukey):
+//   t = b * w, lo = a + t, hi = a - t      (transform.py:160-163)
+__device__ __forceinline__ void bfly_dit(u32 &a, u32 &b, u32 w, u32 wp, u32 p) {
+    u32 t = mul_shoup(b, w, wp, p);
+    u32 x = a;
+    a = add_mod(x, t, p);
+    b = sub_mod(x, t, p);
+}
+
+}  // namespace mc

@@ -1,0 +1,60 @@
+// Host runtime shared by the kernels and the C ABI: field math, twiddle
+// table cache, error reporting and kernel-launch bookkeeping.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+#include "../../include/modconv_b200.h"
+#include "modarith.cuh"
+
+namespace mc {
+
+// ----------------------------------------------------------------- errors
+void set_error(const std::string &msg, int required_two_adicity = -1);
+mc_status fail(mc_status st, const std::string &msg, int required_two_adicity = -1);
+mc_status cuda_fail(cudaError_t e, const char *what);
+void note_launches(int64_t n);
+
+#define MC_CUDA_CHECK(expr)                                    \
+    do {                                                       \
+        cudaError_t _e = (expr);                               \
+        if (_e != cudaSuccess) return ::mc::cuda_fail(_e, #expr); \
+    } while (0)
+
+// ----------------------------------------------------------------- field math
+u64 mulmod(u64 a, u64 b, u64 p);
+u64 powmod(u64 b, u64 e, u64 p);
+bool is_prime_u32(u64 n);
+int two_adicity(u64 p);
+u32 smallest_primitive_root(u32 p);
+Shoup shoup(u32 w, u32 p);
+u32 inv_mod(u32 a, u32 p);
+
+// Validates p (odd prime < 2^31) and log2L <= two-adicity.
+mc_status check_field(u32 p, int log2L);
+
+// ----------------------------------------------------------------- tables
+// Per-(device, p, log2L) constant set.  tf[h + j] = {w_{2h}^j, shoup},
+// ti[h + j] = {w_{2h}^-j, shoup} for 1 <= h < L, 0 <= j < h (the stage
+// slices fwd_stages / inv_stages of transform.py:106-107, concatenated so
+// that one stage's twiddles are contiguous).
+struct FieldTables {
+    u32 p = 0;
+    int log2L = 0;
+    u32 root = 0;       // w_L (field.py:209-224)
+    u32 pinv = 0;       // p^-1 mod 2^32 (Montgomery)
+    Shoup linv;         // L^-1 mod p
+    Shoup linv_mont;    // L^-1 * 2^32 mod p (undoes REDC's 2^-32)
+    uint2 *tf = nullptr;
+    uint2 *ti = nullptr;
+};
+
+// Thread-safe cached lookup (builds on first use; synchronous).
+mc_status get_tables(u32 p, int log2L, const FieldTables **out);
+
+int current_device();
+int sm_count();
+
+}  // namespace mc

@@ -1,0 +1,163 @@
+"""GPU parity of the fused convolution engines (configs 1-3 and the
+reference's own small-size sweeps) against the C oracle and the reference's
+golden fixtures.  Bit-exact: integer residues must be identical."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import P1, P2, P3
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_1609_01010_b200 as mc
+    from gpu_helpers import eval_check, gen_device, sha_row, to_u32_np
+
+
+def _conv(a, b, p, engine):
+    at = torch.from_numpy(np.ascontiguousarray(a, dtype=np.uint32).view(np.int32)).cuda()
+    bt = torch.from_numpy(np.ascontiguousarray(b, dtype=np.uint32).view(np.int32)).cuda()
+    return to_u32_np(mc.conv_batch(at, bt, p, engine=engine))
+
+
+@pytest.mark.parametrize("engine", ["fft_pad", "tft"])
+def test_golden_small_convs(golden_small, engine):
+    for c in golden_small["convs"]:
+        p = c["p"]
+        if c.get("tag") == "all_p_minus_1":
+            u = np.full(c["z1"], p - 1)
+            v = np.full(c["z2"], p - 1)
+        else:
+            u, v = np.array(c["u"]), np.array(c["v"])
+        got = _conv(u[None], v[None], p, engine)[0]
+        assert got.tolist() == c[engine], (p, len(u), len(v), engine)
+
+
+def test_kats(golden_small):
+    k = golden_small["kats"]
+    for c in k["conv17"]:
+        for eng in ("fft_pad", "tft"):
+            got = _conv(np.array([c["u"]]), np.array([c["v"]]), 17, eng)[0]
+            assert got.tolist() == c[eng]
+
+
+@pytest.mark.parametrize("engine", ["fft_pad", "tft"])
+@pytest.mark.parametrize("p", [P2, P3])
+def test_sweep_64x64_vs_oracle(orc, engine, p):
+    """conv_tft vs schoolbook for all 64x64 length pairs
+    (reference tests/test_convolve.py:223-230), batch of 3 rows each."""
+    for z1 in range(1, 65):
+        for z2 in range(1, 65):
+            a = orc.gen_u32(11, 0, z1 * 100 + z2, 3, z1, p)
+            b = orc.gen_u32(11, 1, z1 * 100 + z2, 3, z2, p)
+            want, _, _ = orc.conv_batch(a, b, p, orc.ENGINE_TFT)
+            got = _conv(a, b, p, engine)
+            assert np.array_equal(got, want), (z1, z2, engine)
+
+
+@pytest.mark.parametrize("p", [257, P2])
+def test_sweep_128x128_sampled(orc, p):
+    """Engine sweep over (1..128)^2 (reference tests/test_acceptance.py:85-108),
+    every 3rd z2 to bound runtime; both engines."""
+    for z1 in range(1, 129):
+        for z2 in range(1 + z1 % 3, 129, 3):
+            n = z1 + z2 - 1
+            if (n - 1).bit_length() > orc.two_adicity(p):
+                continue
+            a = orc.gen_u32(12, 0, z1 * 1000 + z2, 2, z1, p)
+            b = orc.gen_u32(12, 1, z1 * 1000 + z2, 2, z2, p)
+            want, _, _ = orc.conv_batch(a, b, p)
+            for eng in ("fft_pad", "tft"):
+                assert np.array_equal(_conv(a, b, p, eng), want), (p, z1, z2, eng)
+
+
+@pytest.mark.parametrize("L", [2**k for k in range(0, 14)])
+@pytest.mark.parametrize("p", [P1, P2, P3])
+def test_power_of_two_boundaries(orc, L, p):
+    """Products exactly at and just past each power-of-two length, plus the
+    all-(p-1) operands that maximise every intermediate."""
+    for n in sorted({L, L + 1, max(1, L - 1)}):
+        for z1 in sorted({1, (n + 1) // 2, n}):
+            z2 = n + 1 - z1
+            if z2 < 1 or (n - 1).bit_length() > 13:
+                continue
+            a = orc.gen_u32(13, 0, n * 7 + z1, 4, z1, p)
+            b = orc.gen_u32(13, 1, n * 7 + z1, 4, z2, p)
+            a[0, :] = p - 1
+            b[0, :] = p - 1
+            b[1, :] = 0
+            want, _, _ = orc.conv_batch(a, b, p)
+            for eng in ("fft_pad", "tft"):
+                assert np.array_equal(_conv(a, b, p, eng), want), (p, n, z1, eng)
+
+
+def test_cfg1_single_product(golden_configs):
+    for cfg in golden_configs["configs"]:
+        if cfg["cfg"] != 1:
+            continue
+        p = cfg["p"]
+        a = gen_device(cfg["seed"], 0, 0, 1, cfg["z1"], p)
+        b = gen_device(cfg["seed"], 1, 0, 1, cfg["z2"], p)
+        for eng in ("fft_pad", "tft"):
+            c = to_u32_np(mc.conv_batch(a, b, p, engine=eng))
+            assert sha_row(c[0]) == cfg["rows"][0]["sha256"], eng
+
+
+def test_cfg2_tft_batch(golden_configs, orc):
+    cfg = next(c for c in golden_configs["configs"] if c["cfg"] == 2 and c["engine"] == "tft")
+    p, z1, z2, B = cfg["p"], cfg["z1"], cfg["z2"], 4096
+    a = gen_device(cfg["seed"], 0, 0, B, z1, p)
+    b = gen_device(cfg["seed"], 1, 0, B, z2, p)
+    c = mc.conv_batch(a, b, p, engine="tft")
+    cn = to_u32_np(c)
+    for rec in cfg["rows"]:
+        assert sha_row(cn[rec["row"]]) == rec["sha256"], rec["row"]
+    rng = np.random.default_rng(2)
+    rows = sorted({0, B - 1, *(rng.integers(0, B, 24).tolist()), *range(0, B, 512),
+                   *range(511, B, 512)})
+    an, bn = to_u32_np(a), to_u32_np(b)
+    want, _, _ = orc.conv_batch(an[rows], bn[rows], p, orc.ENGINE_TFT, threads=8)
+    assert np.array_equal(cn[rows], want)
+    eval_check(a, b, c, p)
+    # the fft_pad engine on the same batch agrees bit for bit
+    assert torch.equal(mc.conv_batch(a, b, p, engine="fft_pad"), c)
+
+
+def test_cfg3_fft_pad_batch(golden_configs, orc):
+    cfg = next(c for c in golden_configs["configs"] if c["cfg"] == 3)
+    p, z1, z2, B = cfg["p"], cfg["z1"], cfg["z2"], 65536
+    a = gen_device(cfg["seed"], 0, 0, B, z1, p)
+    b = gen_device(cfg["seed"], 1, 0, B, z2, p)
+    c = mc.conv_batch(a, b, p, engine="fft_pad")
+    for rec in cfg["rows"]:
+        assert sha_row(to_u32_np(c[rec["row"]])) == rec["sha256"], rec["row"]
+    rng = np.random.default_rng(3)
+    rows = sorted({0, B - 1, *(rng.integers(0, B, 32).tolist()), *range(0, B, 8192),
+                   *range(8191, B, 8192)})
+    idx = torch.tensor(rows, device="cuda")
+    want, _, _ = orc.conv_batch(to_u32_np(a[idx]), to_u32_np(b[idx]), p, threads=8)
+    assert np.array_equal(to_u32_np(c[idx]), want)
+    eval_check(a, b, c, p)
+
+
+def test_strided_rows_and_host_buffers(orc):
+    p = P3
+    a = gen_device(21, 0, 0, 5, 300, p, ld=512)
+    b = gen_device(21, 1, 0, 5, 200, p, ld=256)
+    want, _, _ = orc.conv_batch(to_u32_np(a), to_u32_np(b), p)
+    assert np.array_equal(to_u32_np(mc.conv_batch(a, b, p)), want)
+    ah, bh = a.cpu().pin_memory(), b.cpu().pin_memory()
+    got = mc.conv_batch(ah, bh, p, engine="fft_pad")
+    assert got.device.type == "cpu"
+    assert np.array_equal(got.numpy().view(np.uint32), want)
+
+
+def test_list_api_poly_mul(golden_small):
+    for c in golden_small["poly_mul"]:
+        fp = mc.FourierPrime.from_modulus(c["p"])
+        cnt = mc.OpCounters()
+        r = mc.poly_mul(mc.DensePoly(fp, tuple(c["u"])), mc.DensePoly(fp, tuple(c["v"])),
+                        mc.ConvRequest(fp, engine=c["engine"], counters=cnt))
+        assert list(r.coeffs) == c["out"]
+        assert [cnt.butterflies, cnt.pointwise_muls] == c["counters"]
