@@ -1,0 +1,386 @@
+"""Benchmark of the modular polynomial-multiplication hot path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5]
+                    [--impl mine|reference]
+
+Default workload = BASELINE.json configs[1] (config 2): a batch of 4096
+products of seeded uniform residues mod p = 2013265921, operand lengths
+1500 x 2100 -> 3599 coefficients, truncated-transform engine (conv_tft) at
+L = 4096.  One step = one batched call over the whole batch.  Under
+torchrun each rank multiplies its own 4096-product shard of the seeded stream
+(weak scaling, no collective on the data path); value = all ranks' products
+/ max-over-ranks device time.
+
+Reported: products/s (metric), Gcoeff/s (output coefficients), the HBM
+roofline of the fused kernel (algorithmic bytes 4*(z1+z2+n) per product),
+the integer-pipe view (butterflies/s), the end-to-end number through the
+public API with host (pinned) buffers, and the CPU baseline = the C oracle
+port of the reference path timed on this host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+P1, P2, P3 = 469762049, 998244353, 2013265921
+
+CONFIGS = {
+    1: dict(name="cfg1_single_1024x1024_p469762049_fft_pad", p=P1, z1=1024, z2=1024, batch=1,
+            engine="fft_pad", seed=1),
+    2: dict(name="cfg2_tft_batch4096_1500x2100_p2013265921", p=P3, z1=1500, z2=2100,
+            batch=4096, engine="tft", seed=2),
+    3: dict(name="cfg3_fft_pad_batch65536_4096x4096_p998244353", p=P2, z1=4096, z2=4096,
+            batch=65536, engine="fft_pad", seed=3),
+    4: dict(name="cfg4_fft_pad_batch8_2^22x2^22_p2013265921", p=P3, z1=1 << 22, z2=1 << 22,
+            batch=8, engine="fft_pad", seed=4),
+    5: dict(name="cfg5_three_primes_2^20x2^20_crt", p=0, z1=1 << 20, z2=1 << 20, batch=1,
+            engine="three_primes", seed=5),
+}
+
+L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured", d
+    except Exception:
+        return 6650.0, "fallback", {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out = ""
+        sms, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sms.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sms) if sms else None, "sm_max_mhz": mx,
+                "samples": len(sms), "reasons": sorted(reasons)}
+
+
+def cpu_oracle_rate(cfg, threads: int, target_s: float = 10.0, max_products=None):
+    """Time the C oracle port of the reference path (products/s) on a
+    bounded sample of the workload.  Returns (products/s, sample description)."""
+    from oracle import oracle
+
+    p, z1, z2 = cfg["p"], cfg["z1"], cfg["z2"]
+    if cfg["engine"] == "three_primes":
+        a = oracle.gen_u32(cfg["seed"], 0, 0, 1, z1, 1 << 30)[0]
+        b = oracle.gen_u32(cfg["seed"], 1, 0, 1, z2, 1 << 30)[0]
+        t0 = time.perf_counter()
+        oracle.mul_three_primes(a, b)
+        dt = time.perf_counter() - t0
+        return 1.0 / dt, "1 three-primes product (3 x fft_pad 2^21 + Garner), 1 thread"
+    engine = oracle.ENGINE_TFT if cfg["engine"] == "tft" else oracle.ENGINE_FFT_PAD
+    B = cfg["batch"]
+    # calibrate on a small slice
+    cal = max(1, min(B, threads))
+    a = oracle.gen_u32(cfg["seed"], 0, 0, cal, z1, p)
+    b = oracle.gen_u32(cfg["seed"], 1, 0, cal, z2, p)
+    t0 = time.perf_counter()
+    oracle.conv_batch(a, b, p, engine, threads=threads)
+    per = (time.perf_counter() - t0) / cal
+    nsamp = int(min(B, max(cal, target_s / max(per, 1e-9))))
+    if max_products:
+        nsamp = min(nsamp, max_products)
+    a = oracle.gen_u32(cfg["seed"], 0, 0, nsamp, z1, p)
+    b = oracle.gen_u32(cfg["seed"], 1, 0, nsamp, z2, p)
+    t0 = time.perf_counter()
+    oracle.conv_batch(a, b, p, engine, threads=threads)
+    dt = time.perf_counter() - t0
+    return nsamp / dt, f"{nsamp} of {B} products (rows 0..{nsamp - 1}), {threads} threads"
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def run_reference(args, cfg):
+    """--impl reference: the reference path's CPU implementation (the C
+    oracle port; the reference itself is pure Python and does not travel to
+    the GPU box) with all host threads, same config/metric."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from oracle import oracle
+
+    oracle.lib()
+    threads = host_threads()
+    n = cfg["z1"] + cfg["z2"] - 1
+    rates = []
+    sample = None
+    for i in range(args.warmup + args.steps):
+        r, sample = cpu_oracle_rate(cfg, threads, target_s=args.ref_step_seconds)
+        if i >= args.warmup:
+            rates.append(r)
+    v = statistics.median(rates)
+    line = {
+        "impl": "reference", "metric": "modular poly-mults/sec", "value": v,
+        "unit": "products/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * cfg["batch"] / v, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded splitmix64)",
+        "config": {"workload": cfg["name"], "batch": cfg["batch"], "z1": cfg["z1"],
+                   "z2": cfg["z2"], "n": n, "p": cfg["p"], "engine": cfg["engine"]},
+        "gcoeff_per_s": v * n / 1e9,
+        "cpu_baseline": {"value": v, "unit": "products/s", "cores": threads, "kind": "port",
+                         "sample": sample + " per step; C restatement of the reference "
+                                            "(oracle/modconv_oracle.c)"},
+        "e2e": {"value": v, "unit": "products/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_mine(args, cfg):
+    import torch
+
+    ws, rank, local = _dist()
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    import paper_1609_01010_b200 as mc
+    from paper_1609_01010_b200 import _native, _tensors
+
+    lib = _native.lib()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    p, z1, z2, B = cfg["p"], cfg["z1"], cfg["z2"], cfg["batch"]
+    n = z1 + z2 - 1
+    L = 1 << (n - 1).bit_length()
+    engine = cfg["engine"]
+    stream = torch.cuda.current_stream()
+    sh = _tensors.stream_handle()
+
+    # inputs: this rank's shard of the seeded stream, resident in HBM
+    a = torch.empty((B, z1), dtype=torch.int32, device=dev)
+    b = torch.empty((B, z2), dtype=torch.int32, device=dev)
+    row0 = rank * B
+    hi = p if engine != "three_primes" else (1 << 30)
+    _native.check(lib.mc_gen_u32(cfg["seed"], 0, row0, B, z1, hi, a.data_ptr(), z1, sh))
+    _native.check(lib.mc_gen_u32(cfg["seed"], 1, row0, B, z2, hi, b.data_ptr(), z2, sh))
+    if engine == "three_primes":
+        c = torch.empty((3, n), dtype=torch.int32, device=dev)
+
+        def step():
+            mc.mul_three_primes_tensor(a[0], b[0], out=c)
+    else:
+        c = torch.empty((B, n), dtype=torch.int32, device=dev)
+
+        def step():
+            mc.conv_batch(a, b, p, engine=engine, out=c)
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
+    torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        flush.zero_()
+        step()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    # ---- device-resident timed region: K steps, L2 flushed before each
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    time.sleep(0.3)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    launches0 = _native.launch_count()
+    barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    barrier()
+    launches = _native.launch_count() - launches0
+    clk = clocks.stop()
+    times = [s.elapsed_time(e) for s, e in ev]  # ms
+    total_ms = sum(times)
+    t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if ws > 1:
+        torch.distributed.all_reduce(t_local, op=torch.distributed.ReduceOp.MAX)
+    t_max = float(t_local.item())
+    products = B * args.steps * ws
+    value = products / (t_max / 1e3)
+    ms_step = t_max / args.steps
+
+    # ---- end to end through the public API with pinned host buffers
+    e2e = None
+    if engine != "three_primes":
+        a_h = a.cpu().pin_memory()
+        b_h = b.cpu().pin_memory()
+        c_h = torch.empty((B, n), dtype=torch.int32).pin_memory()
+        for _ in range(max(1, args.warmup)):
+            mc.conv_batch(a_h, b_h, p, engine=engine, out=c_h)
+        torch.cuda.synchronize()
+        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        barrier()
+        for i in range(args.steps):
+            flush.zero_()
+            ev2[i][0].record(stream)
+            mc.conv_batch(a_h, b_h, p, engine=engine, out=c_h)
+            ev2[i][1].record(stream)
+        barrier()
+        t2 = torch.tensor([sum(s.elapsed_time(e) for s, e in ev2)], dtype=torch.float64,
+                          device=dev)
+        if ws > 1:
+            torch.distributed.all_reduce(t2, op=torch.distributed.ReduceOp.MAX)
+        assert torch.equal(c_h.to(dev), c), "e2e output differs from device-resident output"
+        e2e = {"value": products / (float(t2.item()) / 1e3), "unit": "products/s",
+               "h2d_bytes_per_step": 4 * B * (z1 + z2), "d2h_bytes_per_step": 4 * B * n}
+    else:
+        a_h = a[0].cpu().pin_memory()
+        b_h = b[0].cpu().pin_memory()
+        c_h = torch.empty((3, n), dtype=torch.int32).pin_memory()
+        mc.mul_three_primes_tensor(a_h, b_h, out=c).cpu()
+        torch.cuda.synchronize()
+        barrier()
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s0.record(stream)
+        for _ in range(args.steps):
+            flush.zero_()
+            cc = mc.mul_three_primes_tensor(a_h, b_h, out=c)
+            c_h.copy_(cc, non_blocking=True)
+        s1.record(stream)
+        barrier()
+        e2e = {"value": args.steps * ws / (s0.elapsed_time(s1) / 1e3), "unit": "products/s",
+               "h2d_bytes_per_step": 4 * (z1 + z2), "d2h_bytes_per_step": 12 * n}
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    peak, peak_kind, peaks = _peaks()
+    if engine == "three_primes":
+        alg_bytes = 4 * (z1 + z2) + 12 * n
+    else:
+        alg_bytes = 4 * (z1 + z2 + n) * B
+    kern_ms = statistics.mean(times)  # one launch of the fused kernel per step (cfg 1-3)
+    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
+    from paper_1609_01010_b200.transform import full_count, itft_count, tft_count
+
+    if engine == "tft":
+        bf = tft_count(L, z1, n) + tft_count(L, z2, n) + itft_count(L, n)
+        pw = n
+    elif engine == "fft_pad":
+        bf, pw = 3 * full_count(L), L
+    else:
+        bf, pw = 3 * 3 * full_count(L), 3 * L
+    cpu_rate, sample = cpu_oracle_rate(cfg, host_threads(), target_s=args.ref_seconds)
+    line = {
+        "metric": "modular poly-mults/sec", "value": value, "unit": "products/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic (seeded splitmix64 uniform residues, generated on device)",
+        "config": {"workload": cfg["name"], "batch_per_rank": B, "global_batch": B * ws,
+                   "z1": z1, "z2": z2, "n": n, "L": L, "p": p, "engine": engine,
+                   "parallelism": f"dp{ws} (independent products)",
+                   "l2": "flushed (256 MiB write) before every timed step"},
+        "gcoeff_per_s": value * n / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "alg_bytes_per_launch": alg_bytes, "kernel_ms": kern_ms},
+        "int_pipe": {"butterflies_per_product": bf, "pointwise_per_product": pw,
+                     "gbutterflies_per_s": bf * value / ws / 1e9,
+                     "note": "integer-pipe bound; see DESIGN.md for the IMAD roofline"},
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+        "cpu_baseline": {"value": cpu_rate, "unit": "products/s", "cores": host_threads(),
+                         "kind": "port", "sample": sample},
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--ref-seconds", type=float, default=10.0,
+                    help="target CPU seconds of the cpu_baseline sample")
+    ap.add_argument("--ref-step-seconds", type=float, default=2.0,
+                    help="target CPU seconds per --impl reference step")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_mine(args, cfg)
+
+
+if __name__ == "__main__":
+    main()
