@@ -64,12 +64,28 @@ __device__ __forceinline__ int slot_pos(int t, int s) {
     return ((t >> SB) << (SB + 4)) | (s << SB) | (t & ((1 << SB) - 1));
 }
 
-__device__ __forceinline__ uint2 ldtw(const uint2 *tab, int i) { return __ldg(tab + i); }
+// Twiddles are read from the CTA's shared-memory copy of the stage tables:
+// one LDS.64 [Rt + imm] per twiddle (Rt = 8*t precomputed).
+__device__ __forceinline__ uint2 ldtw(const uint2 *tab, int i) { return tab[i]; }
+
+struct Tw {
+    const uint2 *tf;  // shared-memory copy of P.tf
+    const uint2 *ti;  // shared-memory copy of P.ti
+};
 
 // ---------------------------------------------------------------- top pass (forward)
-// Stages with half-size h = H*G, H = 8, 4, 2, 1 on slots (s, s+H).
-template <int K, int NT>
-__device__ __forceinline__ void fwd_top(u32 (&v)[16], int z, int t, const ConvSmallParams &P) {
+// Stages with half-size h = H*G, H = 8, 4, 2, 1 on slots (s, s+H).  All
+// pruning is compile-time: NT (needed output blocks) and ZS = ceil(z/G)
+// rounded up to even (input slots that may hold non-zeros).  A slot
+// offset >= ZS is zero for every lane, so its butterfly is skipped; an
+// offset < ZS whose partner is >= ZS is a multiply-only butterfly.  The one
+// boundary slot that is zero for some lanes only is computed in full (the
+// zeros are real zeros in the registers, so the result is exact).  No
+// runtime branch splits the unrolled butterflies, so ptxas can interleave
+// the independent chains.
+template <int K, int NT, int ZS>
+__device__ __forceinline__ void fwd_top_zs(u32 (&v)[16], int t, const ConvSmallParams &P,
+                                           const Tw &W) {
     constexpr int G = 1 << (K - 4);
     const u32 p = P.p;
 #pragma unroll
@@ -82,27 +98,43 @@ __device__ __forceinline__ void fwd_top(u32 (&v)[16], int z, int t, const ConvSm
             const int sblk = s & ~(2 * H - 1);
             if (sblk >= NT) continue;                 // whole block unneeded
             const bool hi_needed = (sblk + H) < NT;
-            const int jel = t + G * (s & (2 * H - 1));  // offset within the 2h block
-            if (jel < z) {
-                if (jel + h < z) {
-                    if (hi_needed) {
-                        const uint2 w = ldtw(P.tf, h + jel);
-                        bfly_dif(v[s], v[s + H], w.x, w.y, p);
-                    } else {
-                        v[s] = add_mod(v[s], v[s + H], p);  // lo-only add (fold)
-                    }
-                } else if (hi_needed) {
-                    const uint2 w = ldtw(P.tf, h + jel);    // hi input is zero
-                    v[s + H] = mul_shoup(v[s], w.x, w.y, p);
+            const int so = s & (2 * H - 1);           // slot offset within the 2H block
+            if (so >= ZS) continue;                   // both inputs zero
+            const bool hi_zero = so + H >= ZS;
+            if (!hi_zero) {
+                if (hi_needed) {
+                    const uint2 w = ldtw(W.tf, h + t + G * so);
+                    bfly_dif(v[s], v[s + H], w.x, w.y, p);
+                } else {
+                    v[s] = add_mod(v[s], v[s + H], p);  // lo-only add (fold)
                 }
+            } else if (hi_needed) {
+                const uint2 w = ldtw(W.tf, h + t + G * so);
+                v[s + H] = mul_shoup(v[s], w.x, w.y, p);  // hi input is zero
             }
         }
     }
 }
 
+template <int K, int NT>
+__device__ __forceinline__ void fwd_top(u32 (&v)[16], int z, int t, const ConvSmallParams &P,
+                                        const Tw &W) {
+    constexpr int G = 1 << (K - 4);
+    const int zs = (z + G - 1) / G;  // uniform across the launch
+    if (zs <= 2) fwd_top_zs<K, NT, 2>(v, t, P, W);
+    else if (zs <= 4) fwd_top_zs<K, NT, 4>(v, t, P, W);
+    else if (zs <= 6) fwd_top_zs<K, NT, 6>(v, t, P, W);
+    else if (zs <= 8) fwd_top_zs<K, NT, 8>(v, t, P, W);
+    else if (zs <= 10) fwd_top_zs<K, NT, 10>(v, t, P, W);
+    else if (zs <= 12) fwd_top_zs<K, NT, 12>(v, t, P, W);
+    else if (zs <= 14) fwd_top_zs<K, NT, 14>(v, t, P, W);
+    else fwd_top_zs<K, NT, 16>(v, t, P, W);
+}
+
 // ---------------------------------------------------------------- lower passes
 template <int K, int LO, int HI, int SB>
-__device__ __forceinline__ void fwd_lower(u32 (&v)[16], int t, const ConvSmallParams &P) {
+__device__ __forceinline__ void fwd_lower(u32 (&v)[16], int t, const ConvSmallParams &P,
+                                          const Tw &W) {
     const u32 p = P.p;
     const int tpos = slot_pos<SB>(t, 0);
 #pragma unroll
@@ -113,14 +145,15 @@ __device__ __forceinline__ void fwd_lower(u32 (&v)[16], int t, const ConvSmallPa
         for (int s = 0; s < 16; ++s) {
             if ((s >> sbit) & 1) continue;
             const int j = (tpos | (s << SB)) & (h - 1);
-            const uint2 w = ldtw(P.tf, h + j);
+            const uint2 w = ldtw(W.tf, h + j);
             bfly_dif(v[s], v[s | (1 << sbit)], w.x, w.y, p);
         }
     }
 }
 
 template <int K, int LO, int HI, int SB>
-__device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallParams &P) {
+__device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallParams &P,
+                                          const Tw &W) {
     const u32 p = P.p;
     const int tpos = slot_pos<SB>(t, 0);
 #pragma unroll
@@ -131,7 +164,7 @@ __device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallPa
         for (int s = 0; s < 16; ++s) {
             if ((s >> sbit) & 1) continue;
             const int j = (tpos | (s << SB)) & (h - 1);
-            const uint2 w = ldtw(P.ti, h + j);
+            const uint2 w = ldtw(W.ti, h + j);
             bfly_dit(v[s], v[s | (1 << sbit)], w.x, w.y, p);
         }
     }
@@ -142,7 +175,8 @@ __device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallPa
 // level index LV = log2 M (m = M*G elements).
 template <int K, int M, int N, int OFF>
 struct ItftTop {
-    static __device__ __forceinline__ void run(u32 (&v)[16], int t, const ConvSmallParams &P) {
+    static __device__ __forceinline__ void run(u32 (&v)[16], int t, const ConvSmallParams &P,
+                                               const Tw &W) {
         constexpr int G = 1 << (K - 4);
         constexpr int H = M / 2;
         constexpr int LV = (M == 16) ? 4 : (M == 8) ? 3 : (M == 4) ? 2 : 1;
@@ -153,7 +187,7 @@ struct ItftTop {
             // pre: time values of both halves folded into the first half
 #pragma unroll
             for (int s = N; s < H; ++s) v[OFF + s] = add_mod(v[OFF + s], v[OFF + s + H], p);
-            ItftTop<K, H, N, OFF>::run(v, t, P);
+            ItftTop<K, H, N, OFF>::run(v, t, P, W);
             // combine: m*u_i = 2*(h*(u_i + u_{i+h})) - m*u_{i+h}
             const Shoup mm = P.mlev[LV];
 #pragma unroll
@@ -162,22 +196,22 @@ struct ItftTop {
                 v[OFF + s] = sub_mod(add_mod(a, a, p), mul_shoup(v[OFF + s + H], mm, p), p);
             }
         } else {
-            ItftTop<K, H, H, OFF>::run(v, t, P);  // complete first half
+            ItftTop<K, H, H, OFF>::run(v, t, P, W);  // complete first half
             const Shoup mm = P.mlev[LV];
             const Shoup ih = P.hinv[LV];
             constexpr int h = H * G;
 #pragma unroll
             for (int s = N - H; s < H; ++s) {  // cross butterflies
                 u32 a = v[OFF + s], b = v[OFF + s + H];
-                const uint2 w = ldtw(P.tf, h + t + G * s);
+                const uint2 w = ldtw(W.tf, h + t + G * s);
                 u32 d = sub_mod(mul_shoup(a, ih, p), add_mod(b, b, p), p);
                 v[OFF + s + H] = mul_shoup(d, w.x, w.y, p);
                 v[OFF + s] = sub_mod(add_mod(a, a, p), mul_shoup(b, mm, p), p);
             }
-            ItftTop<K, H, N - H, OFF + H>::run(v, t, P);
+            ItftTop<K, H, N - H, OFF + H>::run(v, t, P, W);
 #pragma unroll
             for (int s = 0; s < N - H; ++s) {  // inverse DIT butterflies
-                const uint2 w = ldtw(P.ti, h + t + G * s);
+                const uint2 w = ldtw(W.ti, h + t + G * s);
                 bfly_dit(v[OFF + s], v[OFF + s + H], w.x, w.y, p);
             }
         }
@@ -218,7 +252,7 @@ __device__ __forceinline__ int gblock_of_pass(int t) {
 
 template <int K, int NT, int I>
 __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[16], u32 (&vb)[16],
-                                                int t, const ConvSmallParams &P) {
+                                                int t, const ConvSmallParams &P, const Tw &W) {
     if constexpr (I < Plan<K>::NP) {
         constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         constexpr int SB = Plan<K>::sb(I);
@@ -229,10 +263,10 @@ __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[
         get<SB>(bufA, va, t);
         get<SB>(bufB, vb, t);
         if (NT >= 16 || gblock_of_pass<K, I>(t) < NT) {
-            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(va, t, P);
-            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(vb, t, P);
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(va, t, P, W);
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(vb, t, P, W);
         }
-        fwd_lower_chain<K, NT, I + 1>(bufA, bufB, va, vb, t, P);
+        fwd_lower_chain<K, NT, I + 1>(bufA, bufB, va, vb, t, P, W);
     }
 }
 
@@ -240,17 +274,17 @@ __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[
 // slots are in the top-pass layout.
 template <int K, int NT, int I>
 __device__ __forceinline__ void inv_lower_chain(u32 *buf, u32 (&v)[16], int t,
-                                                const ConvSmallParams &P) {
+                                                const ConvSmallParams &P, const Tw &W) {
     if constexpr (I >= 0) {
         constexpr int SB = Plan<K>::sb(I);
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         if (NT >= 16 || gblock_of_pass<K, I>(t) < NT)
-            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(v, t, P);
+            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(v, t, P, W);
         __syncthreads();
         put<SB>(buf, v, t);
         __syncthreads();
         get<SBnext>(buf, v, t);
-        inv_lower_chain<K, NT, I - 1>(buf, v, t, P);
+        inv_lower_chain<K, NT, I - 1>(buf, v, t, P, W);
     }
 }
 
@@ -260,59 +294,82 @@ struct SmallCfg {
     static constexpr int T = L / 16;
     static constexpr int PPC = T >= 128 ? 1 : 128 / T;  // products per CTA
     static constexpr int THREADS = T * PPC;
-    static constexpr int SMEM = PPC * 2 * L * 4;
+    static constexpr int MINB = THREADS >= 512 ? 1 : 2;  // CTAs per SM (register cap)
+    // shared memory: forward + inverse stage tables, then 2 operand buffers
+    // per product
+    static constexpr int SMEM = 2 * L * 8 + PPC * 2 * L * 4;
 };
 
+// Persistent kernel: each CTA copies the (p, L) stage tables into shared
+// memory once and then walks the batch with a grid stride.
 template <int K, int NT>
-__global__ void __launch_bounds__(SmallCfg<K>::THREADS)
+__global__ void __launch_bounds__(SmallCfg<K>::THREADS, SmallCfg<K>::MINB)
 conv_small_kernel(const ConvSmallParams P) {
     using C = SmallCfg<K>;
     constexpr int L = C::L, T = C::T;
-    extern __shared__ u32 smem[];
-    const int grp = threadIdx.x / T;
-    const int t = threadIdx.x % T;
-    const long long row = (long long)blockIdx.x * C::PPC + grp;
-    const bool valid = row < P.batch;
-    u32 *bufA = smem + grp * 2 * L;
-    u32 *bufB = bufA + L;
-
-    u32 va[16], vb[16];
-    const u32 *ga = P.a + (valid ? row : 0) * P.lda;
-    const u32 *gb = P.b + (valid ? row : 0) * P.ldb;
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {
-        const int x = (s << (K - 4)) | t;
-        va[s] = (valid && x < P.z1) ? __ldcs(ga + x) : 0u;
-        vb[s] = (valid && x < P.z2) ? __ldcs(gb + x) : 0u;
-    }
-
-    fwd_top<K, NT>(va, P.z1, t, P);
-    fwd_top<K, NT>(vb, P.z2, t, P);
-    fwd_lower_chain<K, NT, 0>(bufA, bufB, va, vb, t, P);
-
-    // pointwise product in the last pass's layout, L^-1 folded in
+    extern __shared__ uint4 smem_raw[];
+    uint2 *tf_s = reinterpret_cast<uint2 *>(smem_raw);
+    uint2 *ti_s = tf_s + L;
+    u32 *data = reinterpret_cast<u32 *>(ti_s + L);
     {
-        constexpr int LAST = Plan<K>::NP - 1;
-        constexpr int SB = (Plan<K>::NP == 0) ? (K - 4) : Plan<K>::sb(LAST < 0 ? 0 : LAST);
-#pragma unroll
-        for (int s = 0; s < 16; ++s) {
-            const int x = slot_pos<SB>(t, s);
-            if (NT >= 16 || (x >> (K - 4)) < NT)
-                va[s] = mul_shoup(mont_mul(va[s], vb[s], P.p, P.pinv), P.linv_mont, P.p);
-            else
-                va[s] = 0u;  // time values of the inactive tail: u_j = 0
+        const uint4 *gf = reinterpret_cast<const uint4 *>(P.tf);
+        const uint4 *gi = reinterpret_cast<const uint4 *>(P.ti);
+        uint4 *sf = reinterpret_cast<uint4 *>(tf_s);
+        uint4 *si = reinterpret_cast<uint4 *>(ti_s);
+        for (int i = threadIdx.x; i < L / 2; i += C::THREADS) {
+            sf[i] = __ldg(gf + i);
+            si[i] = __ldg(gi + i);
         }
     }
+    const Tw W{tf_s, ti_s};
+    const int grp = threadIdx.x / T;
+    const int t = threadIdx.x % T;
+    u32 *bufA = data + grp * 2 * L;
+    u32 *bufB = bufA + L;
+    __syncthreads();
 
-    inv_lower_chain<K, NT, Plan<K>::NP - 1>(bufA, va, t, P);
-    ItftTop<K, 16, NT, 0>::run(va, t, P);
-
-    if (valid) {
-        u32 *gc = P.c + row * P.ldc;
+    for (long long base = (long long)blockIdx.x * C::PPC; base < P.batch;
+         base += (long long)gridDim.x * C::PPC) {
+        const long long row = base + grp;
+        const bool valid = row < P.batch;
+        u32 va[16], vb[16];
+        const u32 *ga = P.a + (valid ? row : 0) * P.lda;
+        const u32 *gb = P.b + (valid ? row : 0) * P.ldb;
 #pragma unroll
         for (int s = 0; s < 16; ++s) {
             const int x = (s << (K - 4)) | t;
-            if (x < P.n) __stcs(gc + x, va[s]);
+            va[s] = (valid && x < P.z1) ? __ldcs(ga + x) : 0u;
+            vb[s] = (valid && x < P.z2) ? __ldcs(gb + x) : 0u;
+        }
+
+        fwd_top<K, NT>(va, P.z1, t, P, W);
+        fwd_top<K, NT>(vb, P.z2, t, P, W);
+        fwd_lower_chain<K, NT, 0>(bufA, bufB, va, vb, t, P, W);
+
+        // pointwise product in the last pass's layout, L^-1 folded in
+        {
+            constexpr int LAST = Plan<K>::NP - 1;
+            constexpr int SB = (Plan<K>::NP == 0) ? (K - 4) : Plan<K>::sb(LAST < 0 ? 0 : LAST);
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const int x = slot_pos<SB>(t, s);
+                if (NT >= 16 || (x >> (K - 4)) < NT)
+                    va[s] = mul_shoup(mont_mul(va[s], vb[s], P.p, P.pinv), P.linv_mont, P.p);
+                else
+                    va[s] = 0u;  // time values of the inactive tail: u_j = 0
+            }
+        }
+
+        inv_lower_chain<K, NT, Plan<K>::NP - 1>(bufA, va, t, P, W);
+        ItftTop<K, 16, NT, 0>::run(va, t, P, W);
+
+        if (valid) {
+            u32 *gc = P.c + row * P.ldc;
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const int x = (s << (K - 4)) | t;
+                if (x < P.n) __stcs(gc + x, va[s]);
+            }
         }
     }
 }

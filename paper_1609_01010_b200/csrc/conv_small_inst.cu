@@ -13,14 +13,21 @@ template <int NT>
 static cudaError_t launch_nt(const ConvSmallParams &P, cudaStream_t st) {
     using C = SmallCfg<MC_K>;
     auto kern = conv_small_kernel<MC_K, NT>;
-    static bool attr_done = false;  // benign race: idempotent attribute set
-    if (!attr_done) {
+    static int per_sm = 0;  // benign race: idempotent attribute set / query
+    if (per_sm == 0) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              C::SMEM);
         if (e != cudaSuccess) return e;
-        attr_done = true;
+        int nb = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, C::THREADS, C::SMEM);
+        if (e != cudaSuccess) return e;
+        per_sm = nb > 0 ? nb : 1;
     }
-    const long long grid = (P.batch + C::PPC - 1) / C::PPC;
+    // persistent grid: every resident CTA walks the batch with a grid stride
+    long long grid = (P.batch + C::PPC - 1) / C::PPC;
+    const long long cap = (long long)per_sm * sm_count();
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(P);
     return cudaGetLastError();
 }

@@ -23,17 +23,24 @@ struct Shoup {
     u32 wp;  // floor(w * 2^32 / p)
 };
 
-// [0, 2p) -> [0, p).  Unsigned min: if x < p then x - p wraps above x.
-__device__ __forceinline__ u32 red1(u32 x, u32 p) { return min(x, x - p); }
+// The conditional subtractions below are unsigned minima: if x < p then
+// x - p wraps above x.  They are written with the DPX add-min intrinsic
+// (__viaddmin_u32(a, b, c) = min(a + b, c), one VIADDMNMX on the ALU pipe)
+// so the additions stay off the FMA pipe, which the Shoup products already
+// saturate.
 
+// [0, 2p) -> [0, p)
+__device__ __forceinline__ u32 red1(u32 x, u32 p) { return __viaddmin_u32(x, 0u - p, x); }
+
+// (a + b) mod p for a, b in [0, p): min(a + b, a + b - p)
 __device__ __forceinline__ u32 add_mod(u32 a, u32 b, u32 p) {
-    u32 s = a + b;
-    return min(s, s - p);
+    return __viaddmin_u32(a, b, a + b - p);
 }
 
+// (a - b) mod p for a, b in [0, p): min(a - b, a - b + p)
 __device__ __forceinline__ u32 sub_mod(u32 a, u32 b, u32 p) {
-    u32 d = a - b + p;
-    return min(d, d - p);
+    u32 d = a - b;
+    return __viaddmin_u32(d, p, d);
 }
 
 // x * w mod p in [0, 2p), any 32-bit x.
