@@ -1,0 +1,92 @@
+// Integer-pipe microbenchmarks: the denominators of the integer roofline
+// reported beside the HBM one (configs 1-3 are integer-pipe bound).
+// Each kernel runs 8 independent dependency chains per thread of one
+// instruction kind; rate = lanes * instructions / (cycles * SMs).
+#include <cstdint>
+#include <cstdio>
+
+#include "modarith.cuh"
+#include "runtime.h"
+
+namespace mc {
+
+template <int KIND>
+__global__ void __launch_bounds__(256) ubench_kernel(u32 *out, u32 seed, int iters, u32 p,
+                                                     u32 wp) {
+    u32 x[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = seed * (threadIdx.x + 1) + i * 0x9E3779B9u;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (KIND == 0) x[i] = x[i] * p + wp;                       // IMAD
+                if (KIND == 1) x[i] = __umulhi(x[i], wp) ^ p;              // IMAD.HI (+LOP)
+                if (KIND == 2) x[i] = __viaddmin_u32(x[i], wp, x[i] ^ p);  // VIADDMNMX (+LOP)
+                if (KIND == 3) x[i] = x[i] + wp - p;                       // IADD3
+                if (KIND == 4) x[i] = mul_shoup(x[i], p - 7, wp, p);       // Shoup mul + red
+                if (KIND == 5) {                                           // DIT butterfly
+                    u32 a = x[i], b = x[(i + 1) & 7];
+                    bfly_dit(a, b, p - 7, wp, p);
+                    x[i] = a ^ b;
+                }
+            }
+        }
+    }
+    u32 acc = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc ^= x[i];
+    if (acc == 0x12345678u) out[0] = acc;  // keep the work live
+}
+
+}  // namespace mc
+
+extern "C" {
+
+// rates[k] = thread-level operations per clock per SM for kind k
+// (0 IMAD, 1 IMAD.HI, 2 VIADDMNMX, 3 IADD3, 4 Shoup mul, 5 DIT butterfly),
+// measured at the current SM clock (sm_mhz[0] receives the clock used).
+mc_status mc_ubench_int_pipes(double *rates, int nkinds, double *sm_mhz) {
+    using namespace mc;
+    int dev = current_device();
+    int clk_khz = 0;
+    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+    const int sms = sm_count();
+    u32 *out = nullptr;
+    MC_CUDA_CHECK(cudaMalloc(&out, 4));
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 512, blocks = sms * 8, threads = 256;
+    const u32 p = 2013265921u;
+    const u32 wp = (u32)(((u64)(p - 7) << 32) / p);
+    for (int k = 0; k < nkinds && k < 6; ++k) {
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaEventRecord(e0);
+            switch (k) {
+                case 0: ubench_kernel<0><<<blocks, threads>>>(out, 7, iters, p, wp); break;
+                case 1: ubench_kernel<1><<<blocks, threads>>>(out, 7, iters, p, wp); break;
+                case 2: ubench_kernel<2><<<blocks, threads>>>(out, 7, iters, p, wp); break;
+                case 3: ubench_kernel<3><<<blocks, threads>>>(out, 7, iters, p, wp); break;
+                case 4: ubench_kernel<4><<<blocks, threads>>>(out, 7, iters, p, wp); break;
+                case 5: ubench_kernel<5><<<blocks, threads>>>(out, 7, iters, p, wp); break;
+            }
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double ops = (double)blocks * threads * iters * 16 * 8;
+        const double cycles = ms * 1e-3 * (clk_khz * 1e3);
+        rates[k] = ops / cycles / sms;
+    }
+    if (sm_mhz) *sm_mhz = clk_khz / 1e3;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(out);
+    MC_CUDA_CHECK(cudaGetLastError());
+    return MC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,14 @@
+"""Integer-pipe microbenchmark on cuda:0 -> JSON (ops per clock per SM)."""
+import ctypes, json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_1609_01010_b200 import _native
+torch.cuda.init()
+rates = (ctypes.c_double * 6)()
+mhz = ctypes.c_double()
+_native.check(_native.lib().mc_ubench_int_pipes(rates, 6, ctypes.byref(mhz)))
+names = ["IMAD", "IMAD.HI", "VIADDMNMX", "IADD3", "shoup_mul_red", "dit_butterfly"]
+d = {n: rates[i] for i, n in enumerate(names)}
+d["clock_mhz_attr"] = mhz.value
+d["sms"] = torch.cuda.get_device_properties(0).multi_processor_count
+print(json.dumps(d))
