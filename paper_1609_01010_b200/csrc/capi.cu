@@ -106,7 +106,8 @@ static cudaError_t launch_small(int K, const ConvSmallParams &P, int nt, cudaStr
 // engine 0 = fft_pad, 1 = tft; wrap != 0 => circular convolution of length L
 static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, const u32 *b,
                                long long ldb, int z2, u32 *c, long long ldc, long long batch,
-                               u32 p, cudaStream_t st, int circ_log2L = -1) {
+                               u32 p, cudaStream_t st, int circ_log2L = -1,
+                               bool reduce = false) {
     if (z1 < 1 || z2 < 1) return fail(MC_EINVAL, "inputs must be nonempty");
     if (batch < 0) return fail(MC_EINVAL, "negative batch");
     if (lda < z1 || ldb < z2) return fail(MC_EINVAL, "leading dimension smaller than row length");
@@ -129,6 +130,8 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
     }
     if (K <= kSmallMaxK) {
         ConvSmallParams P = make_params(T, a, lda, z1, b, ldb, z2, c, ldc, n, batch);
+        P.reduce = reduce ? 1 : 0;
+        P.red_wp = (u32)((1ull << 32) / p);
         int nt = 16;
         if (engine == 1 && !circ) {
             const int G = 1 << (K - 4);
@@ -141,7 +144,14 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
         if (e != cudaSuccess) return cuda_fail(e, "conv_small launch");
         return MC_OK;
     }
-    return fourstep_conv(engine, a, lda, z1, b, ldb, z2, c, ldc, batch, p, st, circ_log2L);
+    return fourstep_conv(engine, a, lda, z1, b, ldb, z2, c, ldc, batch, p, st, circ_log2L,
+                         reduce);
+}
+
+// Product mod p of two arbitrary-word vectors (three-primes channels).
+mc_status conv_dispatch_reduced(const u32 *a, int z1, const u32 *b, int z2, u32 *r, u32 p,
+                                cudaStream_t st) {
+    return conv_dispatch(0, a, z1, z1, b, z2, z2, r, (long long)z1 + z2 - 1, 1, p, st, -1, true);
 }
 
 }  // namespace mc

@@ -52,6 +52,8 @@ struct ConvSmallParams {
     const uint2 *ti;   // inverse stage twiddles
     Shoup mlev[5];     // [l] = (2^l * G) mod p, l = 1..4  (m of a top level)
     Shoup hinv[5];     // [l] = (2^(l-1) * G)^-1 mod p    (1/h of a top level)
+    int reduce;        // inputs are arbitrary words: reduce mod p on load
+    u32 red_wp;        // floor(2^32 / p)
 };
 
 // 32-bank conflict-free swizzle for the three access patterns used here:
@@ -219,16 +221,31 @@ struct ItftTop {
 };
 
 // ---------------------------------------------------------------- exchange
-template <int SB>
-__device__ __forceinline__ void put(u32 *buf, const u32 (&v)[16], int t) {
+// Shared-memory address of transform position x.  LaySmall: one transform
+// per buffer (swz).  LayCol<TC>: TC interleaved column transforms, element
+// (x, c) in row x of a TC-wide tile; rows are XOR-permuted so that the
+// 32/TC transform threads sharing a warp always hit distinct bank groups.
+struct LaySmall {
+    __device__ __forceinline__ int operator()(int x) const { return swz(x); }
+};
+
+template <int TC>
+struct LayCol {
+    int c;
+    static constexpr int M = TC >= 32 ? 0 : 32 / TC - 1;
+    __device__ __forceinline__ int operator()(int x) const { return (x ^ ((x >> 4) & M)) * TC + c; }
+};
+
+template <int SB, class Lay = LaySmall>
+__device__ __forceinline__ void put(u32 *buf, const u32 (&v)[16], int t, Lay lay = Lay()) {
 #pragma unroll
-    for (int s = 0; s < 16; ++s) buf[swz(slot_pos<SB>(t, s))] = v[s];
+    for (int s = 0; s < 16; ++s) buf[lay(slot_pos<SB>(t, s))] = v[s];
 }
 
-template <int SB>
-__device__ __forceinline__ void get(const u32 *buf, u32 (&v)[16], int t) {
+template <int SB, class Lay = LaySmall>
+__device__ __forceinline__ void get(const u32 *buf, u32 (&v)[16], int t, Lay lay = Lay()) {
 #pragma unroll
-    for (int s = 0; s < 16; ++s) v[s] = buf[swz(slot_pos<SB>(t, s))];
+    for (int s = 0; s < 16; ++s) v[s] = buf[lay(slot_pos<SB>(t, s))];
 }
 
 // Lower-pass plan for K: up to three passes (bits [8,KL), [4,8), [0,4) with
@@ -288,6 +305,41 @@ __device__ __forceinline__ void inv_lower_chain(u32 *buf, u32 (&v)[16], int t,
     }
 }
 
+// One operand, arbitrary layout: forward lower passes; on exit the slots
+// are in the last lower pass's layout.
+template <int K, int I, class Lay>
+__device__ __forceinline__ void fwd_lower_chain1(u32 *buf, u32 (&v)[16], int t,
+                                                 const ConvSmallParams &P, const Tw &W, Lay lay) {
+    if constexpr (I < Plan<K>::NP) {
+        constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
+        constexpr int SB = Plan<K>::sb(I);
+        __syncthreads();
+        put<SBprev>(buf, v, t, lay);
+        __syncthreads();
+        get<SB>(buf, v, t, lay);
+        fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(v, t, P, W);
+        fwd_lower_chain1<K, I + 1, Lay>(buf, v, t, P, W, lay);
+    }
+}
+
+template <int K, int I, class Lay>
+__device__ __forceinline__ void inv_lower_chain1(u32 *buf, u32 (&v)[16], int t,
+                                                 const ConvSmallParams &P, const Tw &W, Lay lay) {
+    if constexpr (I >= 0) {
+        constexpr int SB = Plan<K>::sb(I);
+        constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
+        inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(v, t, P, W);
+        __syncthreads();
+        put<SB>(buf, v, t, lay);
+        __syncthreads();
+        get<SBnext>(buf, v, t, lay);
+        inv_lower_chain1<K, I - 1, Lay>(buf, v, t, P, W, lay);
+    }
+}
+
+template <int K>
+constexpr int last_sb() { return Plan<K>::NP == 0 ? (K - 4) : Plan<K>::sb(Plan<K>::NP - 1); }
+
 template <int K>
 struct SmallCfg {
     static constexpr int L = 1 << K;
@@ -340,6 +392,13 @@ conv_small_kernel(const ConvSmallParams P) {
             const int x = (s << (K - 4)) | t;
             va[s] = (valid && x < P.z1) ? __ldcs(ga + x) : 0u;
             vb[s] = (valid && x < P.z2) ? __ldcs(gb + x) : 0u;
+        }
+        if (P.reduce) {  // three-primes inputs: any 32-bit word -> residue
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                va[s] = mul_shoup(va[s], 1u, P.red_wp, P.p);
+                vb[s] = mul_shoup(vb[s], 1u, P.red_wp, P.p);
+            }
         }
 
         fwd_top<K, NT>(va, P.z1, t, P, W);

@@ -1,0 +1,115 @@
+// Three-primes integer product over Z (config 5): per-prime products via
+// the convolution engines (inputs reduced on load), then Garner CRT into
+// 3 x 32-bit limbs.  No reference counterpart; see
+// SURVEY.md section 8 a14 for the definition used here.
+#include "fourstep.cuh"
+#include "runtime.h"
+
+namespace mc {
+
+static const u32 kP[3] = {469762049u, 998244353u, 2013265921u};
+
+struct CrtConsts {
+    u32 p1, p2, p3;
+    Shoup inv12;     // p1^-1 mod p2
+    Shoup p1_mod3;   // p1 mod p3
+    Shoup inv123;    // (p1*p2)^-1 mod p3
+    unsigned long long p12;
+};
+
+static CrtConsts crt_consts() {
+    CrtConsts k;
+    k.p1 = kP[0];
+    k.p2 = kP[1];
+    k.p3 = kP[2];
+    k.inv12 = shoup(inv_mod(kP[0] % kP[1], kP[1]), kP[1]);
+    k.p1_mod3 = shoup(kP[0] % kP[2], kP[2]);
+    const u64 p12 = (u64)kP[0] * kP[1];
+    k.inv123 = shoup(inv_mod((u32)(p12 % kP[2]), kP[2]), kP[2]);
+    k.p12 = p12;
+    return k;
+}
+
+// Garner: y2 = (r2 - r1) / p1 mod p2; x12 = r1 + p1*y2 (< p1*p2);
+// y3 = (r3 - x12) / (p1*p2) mod p3; x = x12 + p1*p2*y3 (< 2^90).
+__global__ void crt3_kernel(const u32 *__restrict__ r1, const u32 *__restrict__ r2,
+                            const u32 *__restrict__ r3, u32 *__restrict__ limbs, long long n,
+                            const CrtConsts K) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (long long)gridDim.x * blockDim.x) {
+        const u32 a = __ldcs(r1 + i), b = __ldcs(r2 + i), c = __ldcs(r3 + i);
+        const u32 y2 = mul_shoup(sub_mod(b, a, K.p2), K.inv12, K.p2);  // a < p1 < p2
+        const u32 x12m3 = add_mod(a, mul_shoup(y2, K.p1_mod3, K.p3), K.p3);
+        const u32 y3 = mul_shoup(sub_mod(c, x12m3, K.p3), K.inv123, K.p3);
+        const unsigned long long x12 = (unsigned long long)a + (unsigned long long)K.p1 * y2;
+        const unsigned long long lo = K.p12 * y3;
+        const unsigned long long hi = __umul64hi(K.p12, (unsigned long long)y3);
+        const unsigned long long s = lo + x12;
+        const unsigned long long h = hi + (s < lo ? 1ull : 0ull);
+        __stcs(limbs + i, (u32)s);
+        __stcs(limbs + n + i, (u32)(s >> 32));
+        __stcs(limbs + 2 * n + i, (u32)h);
+    }
+}
+
+static mc_status launch_crt(const u32 *r1, const u32 *r2, const u32 *r3, u32 *limbs, long long n,
+                            cudaStream_t st) {
+    if (n <= 0) return n == 0 ? MC_OK : fail(MC_EINVAL, "negative length");
+    const int thr = 256;
+    long long blocks = std::min<long long>((n + thr - 1) / thr, (long long)sm_count() * 8);
+    crt3_kernel<<<(unsigned)blocks, thr, 0, st>>>(r1, r2, r3, limbs, n, crt_consts());
+    note_launches(1);
+    MC_CUDA_CHECK(cudaGetLastError());
+    return MC_OK;
+}
+
+// product mod kP[k] of arbitrary-word inputs (reduced on load)
+mc_status conv_dispatch_reduced(const u32 *a, int z1, const u32 *b, int z2, u32 *r, u32 p,
+                                cudaStream_t st);
+
+}  // namespace mc
+
+using namespace mc;
+
+extern "C" {
+
+mc_status mc_crt3(const uint32_t *r1, const uint32_t *r2, const uint32_t *r3, uint32_t *limbs,
+                  int64_t n, void *stream) {
+    if (n > 0 && (!r1 || !r2 || !r3 || !limbs)) return fail(MC_EINVAL, "null pointer");
+    return launch_crt(r1, r2, r3, limbs, n, (cudaStream_t)stream);
+}
+
+int64_t mc_three_primes_scratch_words(int32_t z1, int32_t z2) {
+    if (z1 < 1 || z2 < 1) return 0;
+    return 3ll * ((int64_t)z1 + z2 - 1);
+}
+
+mc_status mc_mul_mod_prime_k(const uint32_t *a, int32_t z1, const uint32_t *b, int32_t z2,
+                             uint32_t *r, int k, void *stream) {
+    if (k < 0 || k > 2) return fail(MC_EINVAL, "prime index must be 0, 1 or 2");
+    if (z1 < 1 || z2 < 1) return fail(MC_EINVAL, "inputs must be nonempty");
+    if (!a || !b || !r) return fail(MC_EINVAL, "null pointer");
+    return conv_dispatch_reduced(a, z1, b, z2, r, kP[k], (cudaStream_t)stream);
+}
+
+mc_status mc_mul_three_primes(const uint32_t *a, int32_t z1, const uint32_t *b, int32_t z2,
+                              uint32_t *limbs, uint32_t *scratch, void *stream) {
+    if (z1 < 1 || z2 < 1) return fail(MC_EINVAL, "inputs must be nonempty");
+    if (!a || !b || !limbs) return fail(MC_EINVAL, "null pointer");
+    const long long n = (long long)z1 + z2 - 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    uint32_t *res = scratch;
+    bool own = false;
+    if (!res) {
+        MC_CUDA_CHECK(cudaMallocAsync(&res, sizeof(uint32_t) * 3 * n, st));
+        own = true;
+    }
+    mc_status s = MC_OK;
+    for (int k = 0; k < 3 && s == MC_OK; ++k)
+        s = conv_dispatch_reduced(a, z1, b, z2, res + k * n, kP[k], st);
+    if (s == MC_OK) s = launch_crt(res, res + n, res + 2 * n, limbs, n, st);
+    if (own) cudaFreeAsync(res, st);
+    return s;
+}
+
+}  // extern "C"

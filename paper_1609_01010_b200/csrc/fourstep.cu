@@ -1,11 +1,423 @@
-// Large transforms (L > 8192): four-step decomposition staged through HBM.
+// Four-step large-transform convolution (see fourstep.cuh for the plan).
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "conv_small.cuh"
 #include "fourstep.cuh"
 
 namespace mc {
 
-mc_status fourstep_conv(int, const u32 *, long long, int, const u32 *, long long, int, u32 *,
-                        long long, long long, u32, cudaStream_t, int) {
-    return fail(MC_EUNSUPPORTED, "transform sizes above 8192 are not implemented yet");
+// Twiddle powers w_L^e for any e < L: lo[e & 4095] (plain) times hi[e >> 12]
+// (Shoup pair).  Forward (w) and inverse (w^-1) sets.
+struct TwistTabs {
+    const u32 *lo_f;
+    const uint2 *hi_f;
+    const u32 *lo_i;
+    const uint2 *hi_i;
+    double two32_over_p;  // 2^32 / p, for Shoup companions computed on the fly
+};
+
+struct FourParams {
+    ConvSmallParams cs;  // p, pinv, linv_mont (for the full L), level constants
+    const u32 *a;
+    const u32 *b;
+    u32 *c;
+    long long lda, ldb, ldc;
+    long long z1, z2, n;
+    u32 *Ah;  // scratch: [chunk][L] transformed a, later the product spectrum
+    u32 *Bh;  // scratch: [chunk][L] transformed b
+    long long prod0;  // first product of this chunk
+    int chunk;
+    int reduce;  // inputs are arbitrary words: reduce mod p on load
+    u32 red_wp;  // floor(2^32 / p)
+    TwistTabs tw;
+    const uint2 *col_tf, *col_ti;  // stage tables for the R-point column transforms
+    const uint2 *row_tf, *row_ti;  // stage tables for the C-point row transforms
+};
+
+__device__ __forceinline__ u32 pow_w(const u32 *lo, const uint2 *hi, u32 e, u32 p) {
+    const uint2 h = __ldg(hi + (e >> 12));
+    return mul_shoup(__ldg(lo + (e & 4095)), h.x, h.y, p);
+}
+
+// floor(w * 2^32 / p) via a double estimate and one exact correction step.
+__device__ __forceinline__ u32 shoup_comp(u32 w, u32 p, double two32_over_p) {
+    u32 q = __double2uint_rz((double)w * two32_over_p);
+    long long r = (long long)(((unsigned long long)w << 32) - (unsigned long long)q * p);
+    if (r < 0) --q;
+    else if (r >= (long long)p) ++q;
+    return q;
+}
+
+// ---------------------------------------------------------------- column kernels
+template <int KR>
+struct ColCfg {
+    static constexpr int R = 1 << KR;
+    static constexpr int TC = 16384 >> KR;  // columns per tile (tile = 16K words)
+    static constexpr int THREADS = 1024;
+    static constexpr int G = R / 16;
+    static constexpr int SMEM = R * 8 + 16384 * 4;
+};
+
+template <int KR, int KC>
+__global__ void __launch_bounds__(1024, 1) col_fwd_kernel(const FourParams P) {
+    using C = ColCfg<KR>;
+    constexpr long long Ccols = 1ll << KC;
+    extern __shared__ uint4 smem_raw[];
+    uint2 *tf_s = reinterpret_cast<uint2 *>(smem_raw);
+    u32 *tile = reinterpret_cast<u32 *>(tf_s + C::R);
+    for (int i = threadIdx.x; i < C::R / 2; i += C::THREADS)
+        reinterpret_cast<uint4 *>(tf_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_tf) + i);
+    const Tw W{tf_s, tf_s};
+    const int op = blockIdx.y;
+    const long long prod = P.prod0 + blockIdx.z;
+    const u32 *src = op ? P.b + prod * P.ldb : P.a + prod * P.lda;
+    const long long z = op ? P.z2 : P.z1;
+    u32 *dst = (op ? P.Bh : P.Ah) + (long long)blockIdx.z * (Ccols << KR);
+    const int c = threadIdx.x % C::TC;
+    const int t = threadIdx.x / C::TC;
+    const long long col = (long long)blockIdx.x * C::TC + c;
+    const u32 p = P.cs.p;
+    __syncthreads();
+
+    u32 v[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const long long idx = (long long)(t + C::G * s) * Ccols + col;
+        u32 x = idx < z ? __ldcs(src + idx) : 0u;
+        if (P.reduce) x = mul_shoup(x, 1u, P.red_wp, p);
+        v[s] = x;
+    }
+    const int zrows = (int)((z + Ccols - 1) / Ccols);
+    fwd_top<KR, 16>(v, zrows, t, P.cs, W);
+    LayCol<C::TC> lay{c};
+    fwd_lower_chain1<KR, 0>(tile, v, t, P.cs, W, lay);
+    constexpr int SB = last_sb<KR>();
+#pragma unroll
+    for (int s = 0; s < 16; ++s) dst[(long long)slot_pos<SB>(t, s) * Ccols + col] = v[s];
+}
+
+template <int KR, int KC>
+__global__ void __launch_bounds__(1024, 1) col_inv_kernel(const FourParams P) {
+    using C = ColCfg<KR>;
+    constexpr long long Ccols = 1ll << KC;
+    extern __shared__ uint4 smem_raw[];
+    uint2 *ti_s = reinterpret_cast<uint2 *>(smem_raw);
+    u32 *tile = reinterpret_cast<u32 *>(ti_s + C::R);
+    for (int i = threadIdx.x; i < C::R / 2; i += C::THREADS)
+        reinterpret_cast<uint4 *>(ti_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_ti) + i);
+    const Tw W{ti_s, ti_s};
+    const long long prod = P.prod0 + blockIdx.z;
+    const u32 *src = P.Ah + (long long)blockIdx.z * (Ccols << KR);
+    u32 *dst = P.c + prod * P.ldc;
+    const int c = threadIdx.x % C::TC;
+    const int t = threadIdx.x / C::TC;
+    const long long col = (long long)blockIdx.x * C::TC + c;
+    __syncthreads();
+
+    u32 v[16];
+    constexpr int SB = last_sb<KR>();
+#pragma unroll
+    for (int s = 0; s < 16; ++s) v[s] = src[(long long)slot_pos<SB>(t, s) * Ccols + col];
+    LayCol<C::TC> lay{c};
+    inv_lower_chain1<KR, Plan<KR>::NP - 1>(tile, v, t, P.cs, W, lay);
+    ItftTop<KR, 16, 16, 0>::run(v, t, P.cs, W);
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const long long idx = (long long)(t + C::G * s) * Ccols + col;
+        if (idx < P.n) __stcs(dst + idx, v[s]);
+    }
+}
+
+// ---------------------------------------------------------------- row kernel
+template <int KC>
+struct RowCfg {
+    static constexpr int C = 1 << KC;
+    static constexpr int T = C / 16;
+    static constexpr int PPC = T >= 128 ? 1 : 128 / T;
+    static constexpr int THREADS = T * PPC;
+    static constexpr int SMEM = 2 * C * 8 + PPC * (2 * C * 4 + 32 * 8);
+};
+
+template <int KC>
+__global__ void __launch_bounds__(RowCfg<KC>::THREADS, 2) row_conv_kernel(const FourParams P,
+                                                                          int KR) {
+    using RC = RowCfg<KC>;
+    constexpr int Cn = RC::C, T = RC::T, G = Cn / 16;
+    extern __shared__ uint4 smem_raw[];
+    uint2 *tf_s = reinterpret_cast<uint2 *>(smem_raw);
+    uint2 *ti_s = tf_s + Cn;
+    const int grp = threadIdx.x / T;
+    const int t = threadIdx.x % T;
+    u32 *bufA = reinterpret_cast<u32 *>(ti_s + Cn) + grp * (2 * Cn + 64);
+    u32 *bufB = bufA + Cn;
+    uint2 *beta = reinterpret_cast<uint2 *>(bufB + Cn);  // [0,16) fwd, [16,32) inv
+    {
+        const uint4 *gf = reinterpret_cast<const uint4 *>(P.row_tf);
+        const uint4 *gi = reinterpret_cast<const uint4 *>(P.row_ti);
+        for (int i = threadIdx.x; i < Cn / 2; i += RC::THREADS) {
+            reinterpret_cast<uint4 *>(tf_s)[i] = __ldg(gf + i);
+            reinterpret_cast<uint4 *>(ti_s)[i] = __ldg(gi + i);
+        }
+    }
+    const Tw W{tf_s, ti_s};
+    const u32 p = P.cs.p;
+    const long long R = 1ll << KR;
+    const long long rows = R * P.chunk;
+    __syncthreads();
+
+    for (long long base = (long long)blockIdx.x * RC::PPC; base < rows;
+         base += (long long)gridDim.x * RC::PPC) {
+        const long long gr = base + grp;
+        const bool valid = gr < rows;
+        const long long prod = valid ? gr >> KR : 0;
+        const u32 r = valid ? (u32)(gr & (R - 1)) : 0u;
+        const u32 f1 = __brev(r) >> (32 - KR);
+        if (t < 32) {  // per-row twist factors beta_s = w^(f1*G*s), and inverses
+            const int s = t & 15;
+            const u32 e = f1 * (u32)G * (u32)s;
+            const u32 w = (t < 16) ? pow_w(P.tw.lo_f, P.tw.hi_f, e, p)
+                                   : pow_w(P.tw.lo_i, P.tw.hi_i, e, p);
+            beta[t] = make_uint2(w, shoup_comp(w, p, P.tw.two32_over_p));
+        }
+        // per-thread twist factors alpha_t = w^(f1*t), and inverse
+        const u32 ea = f1 * (u32)t;
+        const u32 af = pow_w(P.tw.lo_f, P.tw.hi_f, ea, p);
+        const u32 ai = pow_w(P.tw.lo_i, P.tw.hi_i, ea, p);
+        const u32 afp = shoup_comp(af, p, P.tw.two32_over_p);
+        const u32 aip = shoup_comp(ai, p, P.tw.two32_over_p);
+        u32 *rowA = P.Ah + prod * (R << KC) + ((long long)r << KC);
+        const u32 *rowB = P.Bh + prod * (R << KC) + ((long long)r << KC);
+        __syncthreads();
+
+        u32 va[16], vb[16];
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const int x = t + G * s;
+            const uint2 bt = beta[s];
+            va[s] = mul_shoup(mul_shoup(valid ? rowA[x] : 0u, af, afp, p), bt.x, bt.y, p);
+            vb[s] = mul_shoup(mul_shoup(valid ? rowB[x] : 0u, af, afp, p), bt.x, bt.y, p);
+        }
+        fwd_top<KC, 16>(va, Cn, t, P.cs, W);
+        fwd_top<KC, 16>(vb, Cn, t, P.cs, W);
+        fwd_lower_chain<KC, 16, 0>(bufA, bufB, va, vb, t, P.cs, W);
+#pragma unroll
+        for (int s = 0; s < 16; ++s)
+            va[s] = mul_shoup(mont_mul(va[s], vb[s], p, P.cs.pinv), P.cs.linv_mont, p);
+        inv_lower_chain<KC, 16, Plan<KC>::NP - 1>(bufA, va, t, P.cs, W);
+        ItftTop<KC, 16, 16, 0>::run(va, t, P.cs, W);
+        if (valid) {
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const uint2 bt = beta[16 + s];
+                rowA[t + G * s] = mul_shoup(mul_shoup(va[s], ai, aip, p), bt.x, bt.y, p);
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------- host side
+struct TwistHost {
+    u32 *lo_f = nullptr, *lo_i = nullptr;
+    uint2 *hi_f = nullptr, *hi_i = nullptr;
+};
+
+static std::mutex g_tw_mu;
+static std::map<std::tuple<int, u32, int>, TwistHost> g_tw;
+
+static mc_status get_twist(const FieldTables *T, TwistTabs *out) {
+    const int K = T->log2L;
+    const u32 p = T->p;
+    const int dev = current_device();
+    auto key = std::make_tuple(dev, p, K);
+    std::lock_guard<std::mutex> lock(g_tw_mu);
+    auto it = g_tw.find(key);
+    if (it == g_tw.end()) {
+        const u64 nlo = 4096, nhi = (K > 12) ? (1ull << (K - 12)) : 1;
+        std::vector<u32> lf(nlo), li(nlo);
+        std::vector<uint2> hf(nhi), hi(nhi);
+        const u32 w = T->root, wi = inv_mod(w, p);
+        u64 a = 1, ai = 1;
+        for (u64 j = 0; j < nlo; ++j) {
+            lf[j] = (u32)a;
+            li[j] = (u32)ai;
+            a = mulmod(a, w, p);
+            ai = mulmod(ai, wi, p);
+        }
+        const u64 step = powmod(w, 4096, p), stepi = powmod(wi, 4096, p);
+        a = ai = 1;
+        for (u64 j = 0; j < nhi; ++j) {
+            Shoup sf = shoup((u32)a, p), si = shoup((u32)ai, p);
+            hf[j] = make_uint2(sf.w, sf.wp);
+            hi[j] = make_uint2(si.w, si.wp);
+            a = mulmod(a, step, p);
+            ai = mulmod(ai, stepi, p);
+        }
+        TwistHost h;
+        cudaError_t e = cudaMalloc(&h.lo_f, 4 * nlo);
+        if (e == cudaSuccess) e = cudaMalloc(&h.lo_i, 4 * nlo);
+        if (e == cudaSuccess) e = cudaMalloc(&h.hi_f, 8 * nhi);
+        if (e == cudaSuccess) e = cudaMalloc(&h.hi_i, 8 * nhi);
+        if (e == cudaSuccess) e = cudaMemcpy(h.lo_f, lf.data(), 4 * nlo, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(h.lo_i, li.data(), 4 * nlo, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(h.hi_f, hf.data(), 8 * nhi, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) e = cudaMemcpy(h.hi_i, hi.data(), 8 * nhi, cudaMemcpyHostToDevice);
+        if (e != cudaSuccess) return cuda_fail(e, "twist table upload");
+        it = g_tw.emplace(key, h).first;
+    }
+    out->lo_f = it->second.lo_f;
+    out->lo_i = it->second.lo_i;
+    out->hi_f = it->second.hi_f;
+    out->hi_i = it->second.hi_i;
+    out->two32_over_p = 4294967296.0 / (double)p;
+    return MC_OK;
+}
+
+template <class KF>
+static cudaError_t prep_kernel(KF kern, int smem, int threads, int *per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm) {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, smem);
+        if (*per_sm < 1) *per_sm = 1;
+    }
+    return e;
+}
+
+template <int KR, int KC>
+static cudaError_t launch_cols(const FourParams &P, bool fwd, cudaStream_t st) {
+    using C = ColCfg<KR>;
+    static bool ready_f = false, ready_i = false;
+    dim3 grid((unsigned)((1u << KC) / C::TC), fwd ? 2u : 1u, (unsigned)P.chunk);
+    if (fwd) {
+        if (!ready_f) {
+            cudaError_t e = prep_kernel(col_fwd_kernel<KR, KC>, C::SMEM, C::THREADS, nullptr);
+            if (e != cudaSuccess) return e;
+            ready_f = true;
+        }
+        col_fwd_kernel<KR, KC><<<grid, C::THREADS, C::SMEM, st>>>(P);
+    } else {
+        if (!ready_i) {
+            cudaError_t e = prep_kernel(col_inv_kernel<KR, KC>, C::SMEM, C::THREADS, nullptr);
+            if (e != cudaSuccess) return e;
+            ready_i = true;
+        }
+        col_inv_kernel<KR, KC><<<grid, C::THREADS, C::SMEM, st>>>(P);
+    }
+    return cudaGetLastError();
+}
+
+template <int KC>
+static cudaError_t launch_rows(const FourParams &P, int KR, cudaStream_t st) {
+    using RC = RowCfg<KC>;
+    static int per_sm = 0;
+    if (!per_sm) {
+        cudaError_t e = prep_kernel(row_conv_kernel<KC>, RC::SMEM, RC::THREADS, &per_sm);
+        if (e != cudaSuccess) return e;
+    }
+    long long work = ((1ll << KR) * P.chunk + RC::PPC - 1) / RC::PPC;
+    long long grid = std::min<long long>(work, (long long)per_sm * sm_count());
+    row_conv_kernel<KC><<<(unsigned)grid, RC::THREADS, RC::SMEM, st>>>(P, KR);
+    return cudaGetLastError();
+}
+
+template <int KC>
+static cudaError_t launch_cols_kc(int KR, const FourParams &P, bool fwd, cudaStream_t st) {
+    switch (KR) {
+        case 4: return launch_cols<4, KC>(P, fwd, st);
+        case 5: return launch_cols<5, KC>(P, fwd, st);
+        case 6: return launch_cols<6, KC>(P, fwd, st);
+        case 7: return launch_cols<7, KC>(P, fwd, st);
+        case 8: return launch_cols<8, KC>(P, fwd, st);
+        case 9: return launch_cols<9, KC>(P, fwd, st);
+        case 10: return launch_cols<10, KC>(P, fwd, st);
+        case 11: return launch_cols<11, KC>(P, fwd, st);
+        case 12: return launch_cols<12, KC>(P, fwd, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+static cudaError_t launch_cols_any(int KC, int KR, const FourParams &P, bool fwd,
+                                   cudaStream_t st) {
+    switch (KC) {
+        case 10: return launch_cols_kc<10>(KR, P, fwd, st);
+        case 11: return launch_cols_kc<11>(KR, P, fwd, st);
+        case 12: return launch_cols_kc<12>(KR, P, fwd, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+static cudaError_t launch_rows_any(int KC, int KR, const FourParams &P, cudaStream_t st) {
+    switch (KC) {
+        case 10: return launch_rows<10>(P, KR, st);
+        case 11: return launch_rows<11>(P, KR, st);
+        case 12: return launch_rows<12>(P, KR, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u32 *b,
+                        long long ldb, int z2, u32 *c, long long ldc, long long batch, u32 p,
+                        cudaStream_t st, int circ_log2L, bool reduce_inputs) {
+    (void)engine;  // the product is exact either way; large L always pads
+    const bool circ = circ_log2L >= 0;
+    const long long n = circ ? (1ll << circ_log2L) : (long long)z1 + z2 - 1;
+    int K = 0;
+    while ((1ll << K) < n) ++K;
+    if (circ) K = circ_log2L;
+    if (K > kFourStepMaxK)
+        return fail(MC_EUNSUPPORTED, "transform size 2^" + std::to_string(K) +
+                                         " exceeds the four-step limit 2^" +
+                                         std::to_string(kFourStepMaxK));
+    const FieldTables *TL, *TR, *TC;
+    mc_status s = get_tables(p, K, &TL);
+    if (s != MC_OK) return s;
+    const int KC = std::min(12, K - 4), KR = K - KC;
+    if ((s = get_tables(p, KR, &TR)) != MC_OK) return s;
+    if ((s = get_tables(p, KC, &TC)) != MC_OK) return s;
+    FourParams P;
+    memset(&P, 0, sizeof(P));
+    if ((s = get_twist(TL, &P.tw)) != MC_OK) return s;
+    P.cs.p = p;
+    P.cs.pinv = TL->pinv;
+    P.cs.linv_mont = TL->linv_mont;  // 1/L for the whole transform
+    P.a = a;
+    P.b = b;
+    P.c = c;
+    P.lda = lda;
+    P.ldb = ldb;
+    P.ldc = ldc;
+    P.z1 = circ ? n : z1;
+    P.z2 = circ ? n : z2;
+    P.n = n;
+    P.reduce = reduce_inputs ? 1 : 0;
+    P.red_wp = (u32)((1ull << 32) / p);
+    P.col_tf = TR->tf;
+    P.col_ti = TR->ti;
+    P.row_tf = TC->tf;
+    P.row_ti = TC->ti;
+    const long long L = 1ll << K;
+    const long long budget_words = 16ll << 20;  // 64 MiB of scratch: stays L2-resident
+    const long long chunk = std::max(1ll, std::min(batch, budget_words / (2 * L)));
+    u32 *scratch = nullptr;
+    MC_CUDA_CHECK(cudaMallocAsync(&scratch, sizeof(u32) * 2 * L * chunk, st));
+    P.Ah = scratch;
+    P.Bh = scratch + L * chunk;
+    mc_status result = MC_OK;
+    for (long long p0 = 0; p0 < batch && result == MC_OK; p0 += chunk) {
+        P.prod0 = p0;
+        P.chunk = (int)std::min(chunk, batch - p0);
+        cudaError_t e = launch_cols_any(KC, KR, P, true, st);
+        if (e == cudaSuccess) e = launch_rows_any(KC, KR, P, st);
+        if (e == cudaSuccess) e = launch_cols_any(KC, KR, P, false, st);
+        note_launches(3);
+        if (e != cudaSuccess) result = cuda_fail(e, "four-step launch");
+    }
+    cudaFreeAsync(scratch, st);
+    return result;
 }
 
 }  // namespace mc

@@ -176,6 +176,11 @@ mc_status get_tables(u32 p, int log2L, const FieldTables **out) {
     u32 li = inv_mod((u32)(L % p), p);
     T->linv = shoup(li, p);
     T->linv_mont = shoup((u32)mulmod(li, (1ull << 32) % p, p), p);
+    if (log2L > kMaxStageTableLog2) {  // large L: four-step sub-tables only
+        g_tabs[key] = T;
+        *out = T;
+        return MC_OK;
+    }
     std::vector<uint2> hf(L > 1 ? L : 2), hi(L > 1 ? L : 2);
     hf[0] = make_uint2(1, (u32)((1ull << 32) / p));
     hi[0] = hf[0];

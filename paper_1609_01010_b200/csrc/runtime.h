@@ -51,6 +51,11 @@ struct FieldTables {
     uint2 *ti = nullptr;
 };
 
+// Stage tables (tf/ti) are only materialised up to this size; larger
+// transforms go through the four-step path whose row/column sub-transforms
+// use their own (small) tables.
+constexpr int kMaxStageTableLog2 = 16;
+
 // Thread-safe cached lookup (builds on first use; synchronous).
 mc_status get_tables(u32 p, int log2L, const FieldTables **out);
 

@@ -54,3 +54,30 @@ def eval_check(a: torch.Tensor, b: torch.Tensor, c: torch.Tensor, p: int, seed: 
             rhs = eval_rows_gpu(a[r0:r1], x, p) * eval_rows_gpu(b[r0:r1], x, p) % p
             bad = torch.nonzero(lhs != rhs).flatten()
             assert bad.numel() == 0, f"eval mismatch at rows {(bad[:8] + r0).tolist()}"
+
+
+def powmod_vec(x: torch.Tensor, e: torch.Tensor, p: int) -> torch.Tensor:
+    """x^e mod p elementwise (int64, x < p < 2^31), by square-and-multiply."""
+    r = torch.ones_like(e)
+    b = x.expand_as(e).clone() % p
+    e = e.clone()
+    while bool((e > 0).any()):
+        odd = (e & 1) == 1
+        r = torch.where(odd, r * b % p, r)
+        b = b * b % p
+        e = e >> 1
+    return r
+
+
+def eval_vec(c: torch.Tensor, x: int, p: int, chunk: int = 1 << 22) -> int:
+    """c(x) mod p for one long residue vector (int32/uint32 on the GPU)."""
+    n = c.numel()
+    acc = 0
+    xt = torch.tensor([x], dtype=torch.int64, device=c.device)
+    for i0 in range(0, n, chunk):
+        i1 = min(n, i0 + chunk)
+        idx = torch.arange(i0, i1, dtype=torch.int64, device=c.device)
+        w = powmod_vec(xt, idx, p)
+        v = (c.reshape(-1)[i0:i1].to(torch.int64) & 0xFFFFFFFF) % p
+        acc = (acc + int(((v * w) % p).sum().item())) % p
+    return acc

@@ -1,0 +1,123 @@
+"""GPU parity of the four-step large-transform path (configs 4 and 5) and the
+three-primes CRT product, against the C oracle, the reference's golden pins
+and size-independent evaluation identities."""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import P1, P2, P3
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_1609_01010_b200 as mc
+    from gpu_helpers import eval_vec, gen_device, to_u32_np
+
+
+@pytest.mark.parametrize("K", [14, 15, 16, 17, 18])
+@pytest.mark.parametrize("p", [P2, P3])
+def test_fourstep_sizes_vs_oracle(orc, K, p):
+    L = 1 << K
+    for n in sorted({L, L - 1, L // 2 + 1, (3 * L) // 4 + 5}):
+        for z1 in sorted({1, (n + 1) // 2, n - 7}):
+            z2 = n + 1 - z1
+            if z1 < 1 or z2 < 1:
+                continue
+            a = orc.gen_u32(40 + K, 0, n + z1, 2, z1, p)
+            b = orc.gen_u32(40 + K, 1, n + z1, 2, z2, p)
+            a[1, :] = p - 1
+            b[1, :] = p - 1
+            want, _, _ = orc.conv_batch(a, b, p, threads=8)
+            at = torch.from_numpy(a.view(np.int32)).cuda()
+            bt = torch.from_numpy(b.view(np.int32)).cuda()
+            for eng in ("fft_pad", "tft"):
+                got = to_u32_np(mc.conv_batch(at, bt, p, engine=eng))
+                assert np.array_equal(got, want), (K, n, z1, eng)
+
+
+@pytest.mark.parametrize("K", [14, 16, 19])
+def test_fourstep_circular(orc, K):
+    p = P3
+    L = 1 << K
+    u = orc.gen_u32(50, 0, K, 1, L, p)[0]
+    v = orc.gen_u32(50, 1, K, 1, L, p)[0]
+    fp = mc.FourierPrime.from_modulus(p)
+    got = mc.circ_conv_fft(u.tolist(), v.tolist(), mc.ConvRequest(fp, engine="fft_pad"))
+    # circular = linear folded mod x^L - 1
+    lin, _, _ = orc.conv_batch(u[None], v[None], p, threads=8)
+    lin = lin[0].astype(np.uint64)
+    fold = lin[:L].copy()
+    fold[: L - 1] = (fold[: L - 1] + lin[L:]) % p
+    assert got == fold.tolist()
+
+
+def test_cfg4_large_products(orc):
+    """Config 4: 8 products of 2^22 x 2^22 mod 2013265921 (L = 2^23).
+    Products 0 and 7 bit-exact vs the oracle; all 8 pass the evaluation
+    identity at two points."""
+    p, z, B = P3, 1 << 22, 8
+    a = gen_device(4, 0, 0, B, z, p)
+    b = gen_device(4, 1, 0, B, z, p)
+    c = mc.conv_batch(a, b, p, engine="fft_pad")
+    torch.cuda.synchronize()
+    for r in (0, B - 1):
+        want, _, _ = orc.conv_batch(to_u32_np(a[r:r + 1]), to_u32_np(b[r:r + 1]), p)
+        assert np.array_equal(to_u32_np(c[r:r + 1]), want), r
+    for r in range(B):
+        for x in (3, 1234567891 % p):
+            assert eval_vec(c[r], x, p) == eval_vec(a[r], x, p) * eval_vec(b[r], x, p) % p, r
+
+
+def test_cfg5_three_primes_pinned(golden_configs, orc):
+    pin = golden_configs["cfg5"]
+    z = pin["z"]
+    a = gen_device(pin["seed"], 0, 0, 1, z, pin["hi"])[0]
+    b = gen_device(pin["seed"], 1, 0, 1, z, pin["hi"])[0]
+    limbs = mc.mul_three_primes_tensor(a, b)
+    ln = to_u32_np(limbs)
+    assert hashlib.sha256(ln.tobytes()).hexdigest() == pin["limbs_sha256"]
+    assert [str(x) for x in orc.limbs_to_ints(ln[:, :4])] == pin["head"]
+    assert [str(x) for x in orc.limbs_to_ints(ln[:, -4:])] == pin["tail"]
+    # per-prime channels match the reference's per-prime products
+    from paper_1609_01010_b200 import _native, _tensors
+
+    for k, p in enumerate((P1, P2, P3)):
+        r = torch.empty(2 * z - 1, dtype=torch.int32, device="cuda")
+        _native.check(_native.lib().mc_mul_mod_prime_k(a.data_ptr(), z, b.data_ptr(), z,
+                                                        r.data_ptr(), k,
+                                                        _tensors.stream_handle()))
+        assert hashlib.sha256(to_u32_np(r).tobytes()).hexdigest() == \
+            pin["per_prime"][str(p)]["sha256"], p
+
+
+@pytest.mark.parametrize("z1,z2", [(1, 1), (1, 9), (5, 3), (300, 200), (4096, 4096),
+                                    (5000, 3), (20000, 17000)])
+def test_three_primes_small_exact(orc, z1, z2):
+    rng = np.random.default_rng(z1 * 7 + z2)
+    a = rng.integers(0, 1 << 30, z1, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, 1 << 30, z2, dtype=np.uint64).astype(np.uint32)
+    a[0] = (1 << 30) - 1
+    b[-1] = (1 << 30) - 1
+    got = mc.mul_three_primes(a.tolist(), b.tolist())
+    want = orc.limbs_to_ints(orc.mul_three_primes(a, b))
+    assert got == want
+    if z1 * z2 <= 100000:
+        exact = [0] * (z1 + z2 - 1)
+        for i, x in enumerate(a.tolist()):
+            for j, y in enumerate(b.tolist()):
+                exact[i + j] += x * y
+        assert got == exact
+
+
+def test_crt3_kernel_edges(orc):
+    n = 1000
+    rng = np.random.default_rng(5)
+    rs = [rng.integers(0, p, n, dtype=np.uint64).astype(np.uint32) for p in (P1, P2, P3)]
+    for r, p in zip(rs, (P1, P2, P3)):
+        r[:3] = [0, p - 1, 1]
+    t = [torch.from_numpy(r.view(np.int32)).cuda() for r in rs]
+    got = to_u32_np(mc.crt3(*t))
+    assert np.array_equal(got, orc.crt3(*rs))
