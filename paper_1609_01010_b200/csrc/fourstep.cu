@@ -276,6 +276,20 @@ static mc_status get_twist(const FieldTables *T, TwistTabs *out) {
     return MC_OK;
 }
 
+mc_status get_twist_tables(u32 p, int K, const u32 **lo_f, const uint2 **hi_f, const u32 **lo_i,
+                           const uint2 **hi_i) {
+    const FieldTables *T;
+    mc_status s = get_tables(p, K, &T);
+    if (s != MC_OK) return s;
+    TwistTabs tw;
+    if ((s = get_twist(T, &tw)) != MC_OK) return s;
+    *lo_f = tw.lo_f;
+    *hi_f = tw.hi_f;
+    *lo_i = tw.lo_i;
+    *hi_i = tw.hi_i;
+    return MC_OK;
+}
+
 template <class KF>
 static cudaError_t prep_kernel(KF kern, int smem, int threads, int *per_sm) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

@@ -1,0 +1,389 @@
+// Standalone transforms with the reference's exact semantics (API parity,
+// SURVEY.md 8f row 1):
+//   mc_ntt   transform.py:167-196  natural order in and out, inverse / L
+//   mc_tft   transform.py:379-448  first n bit-reversed spectral values
+//   mc_itft  transform.py:451-529  L * u_i, i < n, from n spectral values
+//
+// Level-scheduled on global memory: one launch per butterfly level over
+// all rows of the batch (any L up to 2^27, limited by the field).  Twiddles
+// w_{2h}^j = w_L^(j*L/2h) come from the two-level power tables of the
+// four-step path (lo[e & 4095] * hi[e >> 12]); the variable-twiddle
+// products use Montgomery multiplication with the twiddle in Montgomery
+// form.  These entry points exist for call-compatibility of
+// moddft/tft/itft; the convolution hot path never uses them.
+#include <vector>
+
+#include "fourstep.cuh"
+#include "runtime.h"
+
+namespace mc {
+
+struct TfmTabs {
+    const u32 *lo_f;
+    const uint2 *hi_f;
+    const u32 *lo_i;
+    const uint2 *hi_i;
+};
+
+// defined in fourstep.cu
+mc_status get_twist_tables(u32 p, int K, const u32 **lo_f, const uint2 **hi_f, const u32 **lo_i,
+                           const uint2 **hi_i);
+
+struct TfmParams {
+    u32 *w;           // work rows [batch][ldw]
+    long long ldw;
+    long long batch;
+    int K;            // log2 L
+    u32 p, pinv;
+    u32 r2;           // 2^64 mod p (to enter Montgomery form)
+    TfmTabs tb;
+};
+
+__device__ __forceinline__ u32 tw_pow(const u32 *lo, const uint2 *hi, u32 e, u32 p) {
+    const uint2 h = __ldg(hi + (e >> 12));
+    return mul_shoup(__ldg(lo + (e & 4095)), h.x, h.y, p);
+}
+
+// x * w mod p, w canonical (variable): Montgomery with an R^2 correction.
+__device__ __forceinline__ u32 mulv(u32 x, u32 w, const TfmParams &P) {
+    return mont_mul(mont_mul(x, w, P.p, P.pinv), P.r2, P.p, P.pinv);
+}
+
+// w_{2h}^j for the stage with half-size h (both directions)
+__device__ __forceinline__ u32 stage_tw(const TfmParams &P, long long h, long long j, bool inv) {
+    const u32 e = (u32)(j << (P.K - 1 - __ffsll(h) + 1));  // j * L / (2h)
+    return inv ? tw_pow(P.tb.lo_i, P.tb.hi_i, e, P.p) : tw_pow(P.tb.lo_f, P.tb.hi_f, e, P.p);
+}
+
+// --- moddft -------------------------------------------------------------
+__global__ void bitrev_copy_kernel(const u32 *x, u32 *w, long long ldw, long long batch, int K) {
+    const long long L = 1ll << K;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < L * batch;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i >> K, j = i & (L - 1);
+        const long long rj = K ? (long long)(__brevll((unsigned long long)j) >> (64 - K)) : 0;
+        w[r * ldw + rj] = x[r * L + j];
+    }
+}
+
+__global__ void dit_stage_kernel(TfmParams P, long long h, int inv) {
+    const long long L = 1ll << P.K, half = L >> 1;
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < half * P.batch;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / half, k = i % half;
+        const long long j = k & (h - 1), blk = k / h;
+        u32 *row = P.w + r * P.ldw;
+        const long long lo = blk * 2 * h + j, hi = lo + h;
+        const u32 t = mulv(row[hi], stage_tw(P, h, j, inv), P);
+        const u32 u = row[lo];
+        row[lo] = add_mod(u, t, P.p);
+        row[hi] = sub_mod(u, t, P.p);
+    }
+}
+
+__global__ void scale_copy_kernel(const u32 *w, long long ldw, u32 *y, long long n, long long ldy,
+                                  long long batch, u32 s, u32 sp, u32 p, int do_scale) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n * batch;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / n, j = i % n;
+        u32 v = w[r * ldw + j];
+        if (do_scale) v = mul_shoup(v, s, sp, p);
+        y[r * ldy + j] = v;
+    }
+}
+
+// --- truncated forward ----------------------------------------------------
+// One DIF level (block size m = 2h) of the reference recursion
+// (transform.py:379-418), all computed blocks (start < n) at once.
+__global__ void tft_level_kernel(TfmParams P, long long h, long long z, long long n) {
+    const long long m = 2 * h;
+    const long long nblk = (n + m - 1) / m;
+    const long long per = nblk * h;
+    const long long zz = z < m ? z : m;  // every computed block holds min(z, m) inputs
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < per * P.batch;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / per, k = i % per;
+        const long long b = (k / h) * m, j = k % h;
+        if (j >= zz) continue;  // both inputs known zero
+        u32 *row = P.w + r * P.ldw;
+        const bool b_zero = j + h >= zz;
+        const bool hi_needed = b + h < n;
+        const long long lo = b + j, hi = lo + h;
+        if (hi_needed) {
+            const u32 w = stage_tw(P, h, j, false);
+            if (b_zero) {
+                row[hi] = mulv(row[lo], w, P);
+            } else {
+                const u32 a = row[lo], c = row[hi];
+                row[lo] = add_mod(a, c, P.p);
+                row[hi] = mulv(sub_mod(a, c, P.p), w, P);
+            }
+        } else if (!b_zero) {
+            row[lo] = add_mod(row[lo], row[hi], P.p);
+        }
+    }
+}
+
+__global__ void load_pad_kernel(const u32 *x, long long ldx, long long z, u32 *w, long long ldw,
+                                long long L, long long batch, u32 p, u32 red_wp) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < L * batch;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / L, j = i % L;
+        w[r * ldw + j] = j < z ? mul_shoup(x[r * ldx + j], 1u, red_wp, p) : 0u;
+    }
+}
+
+// --- truncated inverse ----------------------------------------------------
+// Chain of the van der Hoeven recursion (transform.py:451-489): complete
+// sub-blocks are plain inverse DITs (done first, all at once); the partial
+// path is walked top-down (cross / pre-add) and then bottom-up (DIT /
+// combine).
+struct Block {
+    long long off, size;
+};
+
+constexpr int kMaxBlocks = 40;
+
+struct BlockList {
+    Block b[kMaxBlocks];
+    long long pre[kMaxBlocks + 1];  // prefix sums of per-stage butterflies
+    int nb;
+};
+
+__global__ void blocks_dit_stage_kernel(TfmParams P, BlockList BL, long long h) {
+    const long long total = BL.pre[BL.nb];
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < total * P.batch;
+         i += (long long)gridDim.x * blockDim.x) {
+        const long long r = i / total, k = i % total;
+        int q = 0;
+        while (k >= BL.pre[q + 1]) ++q;
+        const long long kk = k - BL.pre[q];
+        const long long j = kk & (h - 1), blk = kk / h;
+        u32 *row = P.w + r * P.ldw + BL.b[q].off;
+        const long long lo = blk * 2 * h + j, hi = lo + h;
+        const u32 t = mulv(row[hi], stage_tw(P, h, j, true), P);
+        const u32 u = row[lo];
+        row[lo] = add_mod(u, t, P.p);
+        row[hi] = sub_mod(u, t, P.p);
+    }
+}
+
+// kind: 0 pre-add, 1 combine, 2 cross, 3 DIT; range [i0, i1) of offsets
+__global__ void chain_op_kernel(TfmParams P, long long off, long long h, long long i0,
+                                long long i1, int kind, Shoup m_mod, Shoup inv_h) {
+    const long long cnt = i1 - i0;
+    if (cnt <= 0) return;
+    const u32 p = P.p;
+    for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < cnt * P.batch;
+         t += (long long)gridDim.x * blockDim.x) {
+        const long long r = t / cnt, i = i0 + t % cnt;
+        u32 *row = P.w + r * P.ldw + off;
+        const long long lo = i, hi = i + h;
+        if (kind == 0) {
+            row[lo] = add_mod(row[lo], row[hi], p);
+        } else if (kind == 1) {
+            const u32 a = row[lo];
+            row[lo] = sub_mod(add_mod(a, a, p), mul_shoup(row[hi], m_mod, p), p);
+        } else if (kind == 2) {
+            const u32 a = row[lo], b = row[hi];
+            const u32 d = sub_mod(mul_shoup(a, inv_h, p), add_mod(b, b, p), p);
+            row[hi] = mulv(d, stage_tw(P, h, i, false), P);
+            row[lo] = sub_mod(add_mod(a, a, p), mul_shoup(b, m_mod, p), p);
+        } else {
+            const u32 tt = mulv(row[hi], stage_tw(P, h, i, true), P);
+            const u32 a = row[lo];
+            row[lo] = add_mod(a, tt, p);
+            row[hi] = sub_mod(a, tt, p);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- host helpers
+static unsigned grid_for(long long work) {
+    long long g = (work + 255) / 256;
+    long long cap = (long long)sm_count() * 16;
+    if (g > cap) g = cap;
+    return (unsigned)(g < 1 ? 1 : g);
+}
+
+static mc_status tfm_setup(u32 p, int K, TfmParams *P) {
+    const FieldTables *T;
+    mc_status s = get_tables(p, K, &T);
+    if (s != MC_OK) return s;
+    if ((s = get_twist_tables(p, K, &P->tb.lo_f, &P->tb.hi_f, &P->tb.lo_i, &P->tb.hi_i)) != MC_OK)
+        return s;
+    P->K = K;
+    P->p = p;
+    P->pinv = T->pinv;
+    const u64 r1 = (1ull << 32) % p;
+    P->r2 = (u32)mulmod(r1, r1, p);
+    return MC_OK;
+}
+
+}  // namespace mc
+
+using namespace mc;
+
+extern "C" {
+
+mc_status mc_ntt(const uint32_t *x, uint32_t *y, int32_t log2L, int64_t batch, uint32_t p,
+                 int inverse, void *stream) {
+    if (log2L < 0 || log2L > 30) return fail(MC_EINVAL, "bad transform size");
+    if (batch < 0) return fail(MC_EINVAL, "negative batch");
+    TfmParams P;
+    memset(&P, 0, sizeof(P));
+    mc_status s = tfm_setup(p, log2L, &P);
+    if (s != MC_OK || batch == 0) return s;
+    if (!x || !y) return fail(MC_EINVAL, "null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    const long long L = 1ll << log2L;
+    u32 *w = nullptr;
+    MC_CUDA_CHECK(cudaMallocAsync(&w, 4ull * L * batch, st));
+    P.w = w;
+    P.ldw = L;
+    P.batch = batch;
+    bitrev_copy_kernel<<<grid_for(L * batch), 256, 0, st>>>(x, w, L, batch, log2L);
+    for (long long h = 1; h < L; h <<= 1)
+        dit_stage_kernel<<<grid_for(L / 2 * batch), 256, 0, st>>>(P, h, inverse ? 1 : 0);
+    const FieldTables *T;
+    get_tables(p, log2L, &T);
+    scale_copy_kernel<<<grid_for(L * batch), 256, 0, st>>>(w, L, y, L, L, batch, T->linv.w,
+                                                           T->linv.wp, p, inverse ? 1 : 0);
+    note_launches(2 + log2L);
+    cudaFreeAsync(w, st);
+    MC_CUDA_CHECK(cudaGetLastError());
+    return MC_OK;
+}
+
+mc_status mc_tft(const uint32_t *x, int32_t z, uint32_t *y, int32_t n, int32_t log2L,
+                 int64_t batch, uint32_t p, void *stream) {
+    if (log2L < 0 || log2L > 30) return fail(MC_EINVAL, "bad transform size");
+    const long long L = 1ll << log2L;
+    if (z < 1) return fail(MC_EINVAL, "input must be nonempty");
+    if (z > n) return fail(MC_EINVAL, "input length exceeds output count");
+    if (n > L) return fail(MC_EINVAL, "output count exceeds transform size");
+    if (batch < 0) return fail(MC_EINVAL, "negative batch");
+    TfmParams P;
+    memset(&P, 0, sizeof(P));
+    mc_status s = tfm_setup(p, log2L, &P);
+    if (s != MC_OK || batch == 0) return s;
+    if (!x || !y) return fail(MC_EINVAL, "null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    u32 *w = nullptr;
+    MC_CUDA_CHECK(cudaMallocAsync(&w, 4ull * L * batch, st));
+    P.w = w;
+    P.ldw = L;
+    P.batch = batch;
+    load_pad_kernel<<<grid_for(L * batch), 256, 0, st>>>(x, z, z, w, L, L, batch, p,
+                                                         (u32)((1ull << 32) / p));
+    int launches = 2;
+    for (long long h = L >> 1; h >= 1; h >>= 1) {
+        const long long nblk = (n + 2 * h - 1) / (2 * h);
+        tft_level_kernel<<<grid_for(nblk * h * batch), 256, 0, st>>>(P, h, z, n);
+        ++launches;
+    }
+    scale_copy_kernel<<<grid_for((long long)n * batch), 256, 0, st>>>(w, L, y, n, n, batch, 0, 0,
+                                                                      p, 0);
+    note_launches(launches);
+    cudaFreeAsync(w, st);
+    MC_CUDA_CHECK(cudaGetLastError());
+    return MC_OK;
+}
+
+mc_status mc_itft(const uint32_t *xhat, uint32_t *y, int32_t n, int32_t log2L, int64_t batch,
+                  uint32_t p, void *stream) {
+    if (log2L < 0 || log2L > 30) return fail(MC_EINVAL, "bad transform size");
+    const long long L = 1ll << log2L;
+    if (n < 1) return fail(MC_EINVAL, "spectral input must be nonempty");
+    if (n > L) return fail(MC_EINVAL, "input length exceeds transform size");
+    if (batch < 0) return fail(MC_EINVAL, "negative batch");
+    TfmParams P;
+    memset(&P, 0, sizeof(P));
+    mc_status s = tfm_setup(p, log2L, &P);
+    if (s != MC_OK || batch == 0) return s;
+    if (!xhat || !y) return fail(MC_EINVAL, "null pointer");
+    cudaStream_t st = (cudaStream_t)stream;
+    u32 *w = nullptr;
+    MC_CUDA_CHECK(cudaMallocAsync(&w, 4ull * L * batch, st));
+    P.w = w;
+    P.ldw = L;
+    P.batch = batch;
+    load_pad_kernel<<<grid_for(L * batch), 256, 0, st>>>(xhat, n, n, w, L, L, batch, p,
+                                                         (u32)((1ull << 32) / p));
+    int launches = 2;
+    // Walk the partial path: nodes (off, m, n) with 0 < n < m.
+    struct Node {
+        long long off, m, n;
+    };
+    std::vector<Node> chain;
+    BlockList BL;
+    memset(&BL, 0, sizeof(BL));
+    {
+        long long off = 0, m = L, nn = n;
+        while (m > 1 && nn > 0) {
+            if (nn == m) {  // complete: plain inverse DIT of the whole block
+                BL.b[BL.nb++] = Block{off, m};
+                break;
+            }
+            const long long h = m >> 1;
+            chain.push_back(Node{off, m, nn});
+            if (nn <= h) {
+                m = h;
+            } else {
+                BL.b[BL.nb++] = Block{off, h};  // complete first half
+                off += h;
+                nn -= h;
+                m = h;
+            }
+        }
+    }
+    // 1. complete blocks, stage by stage (bottom-up)
+    for (long long h = 1; h < L; h <<= 1) {
+        BlockList sub;
+        memset(&sub, 0, sizeof(sub));
+        for (int q = 0; q < BL.nb; ++q)
+            if (BL.b[q].size >= 2 * h) {
+                sub.b[sub.nb] = BL.b[q];
+                sub.pre[sub.nb + 1] = sub.pre[sub.nb] + BL.b[q].size / 2;
+                ++sub.nb;
+            }
+        if (!sub.nb) break;
+        blocks_dit_stage_kernel<<<grid_for(sub.pre[sub.nb] * batch), 256, 0, st>>>(P, sub, h);
+        ++launches;
+    }
+    // 2. down the chain: cross (n > h) or pre-add (n <= h)
+    for (const Node &nd : chain) {
+        const long long h = nd.m >> 1;
+        const Shoup mm = shoup((u32)(nd.m % p), p);
+        const Shoup ih = shoup(inv_mod((u32)(h % p), p), p);
+        if (nd.n > h)
+            chain_op_kernel<<<grid_for((2 * h - nd.n) * batch), 256, 0, st>>>(
+                P, nd.off, h, nd.n - h, h, 2, mm, ih);
+        else
+            chain_op_kernel<<<grid_for((h - nd.n) * batch), 256, 0, st>>>(P, nd.off, h, nd.n, h,
+                                                                          0, mm, ih);
+        ++launches;
+    }
+    // 3. up the chain: DIT (n > h) or combine (n <= h)
+    for (auto it = chain.rbegin(); it != chain.rend(); ++it) {
+        const Node &nd = *it;
+        const long long h = nd.m >> 1;
+        const Shoup mm = shoup((u32)(nd.m % p), p);
+        const Shoup ih = shoup(inv_mod((u32)(h % p), p), p);
+        if (nd.n > h)
+            chain_op_kernel<<<grid_for((nd.n - h) * batch), 256, 0, st>>>(P, nd.off, h, 0,
+                                                                          nd.n - h, 3, mm, ih);
+        else
+            chain_op_kernel<<<grid_for(nd.n * batch), 256, 0, st>>>(P, nd.off, h, 0, nd.n, 1, mm,
+                                                                    ih);
+        ++launches;
+    }
+    scale_copy_kernel<<<grid_for((long long)n * batch), 256, 0, st>>>(w, L, y, n, n, batch, 0, 0,
+                                                                      p, 0);
+    note_launches(launches);
+    cudaFreeAsync(w, st);
+    MC_CUDA_CHECK(cudaGetLastError());
+    return MC_OK;
+}
+
+}  // extern "C"

@@ -8,3 +8,5 @@ for c in 2 1 3; do python -c "
 import json; d=json.load(open('gpurun_out/bench_cfg$c.json'))
 print('cfg$c', round(d['value']), d['unit'], 'kernel_ms', round(d['roofline']['kernel_ms'],4), 'frac', round(d['roofline']['frac'],4), 'e2e', round(d['e2e']['value']), 'clk', d['clocks'])
 "; done
+python bench.py --config 4 --steps 5 --warmup 3 --ref-seconds 1 > gpurun_out/bench_cfg4.json 2>&1
+python bench.py --config 5 --steps 5 --warmup 3 --ref-seconds 1 > gpurun_out/bench_cfg5.json 2>&1
