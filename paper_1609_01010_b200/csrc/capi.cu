@@ -132,6 +132,20 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
         ConvSmallParams P = make_params(T, a, lda, z1, b, ldb, z2, c, ldc, n, batch);
         P.reduce = reduce ? 1 : 0;
         P.red_wp = (u32)((1ull << 32) / p);
+        // TMA row prefetch: one product per CTA, 16-byte aligned rows, fits in smem
+        {
+            const bool one_per_cta = (1 << K) / 16 >= 128;
+            const bool aligned = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) &&
+                                 (lda % 4 == 0) && (ldb % 4 == 0);
+            const int za16 = z1 & ~3, zb16 = z2 & ~3;
+            const long long smem = 2ll * (1 << K) * 8 + 2ll * (1 << K) * 4 + 16 +
+                                   4ll * (za16 + zb16);  // upper bound (tables in smem)
+            if (one_per_cta && aligned && smem <= 227 * 1024 && batch > 0) {
+                P.tma = 1;
+                P.za16 = za16;
+                P.zb16 = zb16;
+            }
+        }
         int nt = 16;
         if (engine == 1 && !circ) {
             const int G = 1 << (K - 4);

@@ -13,22 +13,28 @@ template <int NT>
 static cudaError_t launch_nt(const ConvSmallParams &P, cudaStream_t st) {
     using C = SmallCfg<MC_K>;
     auto kern = conv_small_kernel<MC_K, NT>;
-    static int per_sm = 0;  // benign race: idempotent attribute set / query
-    if (per_sm == 0) {
+    // dynamic shared memory: tables + data (+ TMA staging of both rows)
+    const int smem = C::SMEM + (P.tma ? 16 + 4 * (P.za16 + P.zb16) : 0);
+    static int attr_smem = 0, per_sm = 0, per_sm_smem = -1;  // benign races: idempotent
+    if (smem > attr_smem) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             C::SMEM);
+                                             smem);
         if (e != cudaSuccess) return e;
+        attr_smem = smem;
+    }
+    if (per_sm_smem != smem) {
         int nb = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, C::THREADS, C::SMEM);
+        cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, C::THREADS, smem);
         if (e != cudaSuccess) return e;
         per_sm = nb > 0 ? nb : 1;
+        per_sm_smem = smem;
     }
     // persistent grid: every resident CTA walks the batch with a grid stride
     long long grid = (P.batch + C::PPC - 1) / C::PPC;
     const long long cap = (long long)per_sm * sm_count();
     if (grid > cap) grid = cap;
     if (grid < 1) grid = 1;
-    kern<<<(unsigned)grid, C::THREADS, C::SMEM, st>>>(P);
+    kern<<<(unsigned)grid, C::THREADS, smem, st>>>(P);
     return cudaGetLastError();
 }
 
