@@ -36,6 +36,7 @@
 // the position-level model checked against the oracle.
 #pragma once
 #include "modarith.cuh"
+#include "tma.cuh"
 
 namespace mc {
 
@@ -54,6 +55,9 @@ struct ConvSmallParams {
     Shoup hinv[5];     // [l] = (2^(l-1) * G)^-1 mod p    (1/h of a top level)
     int reduce;        // inputs are arbitrary words: reduce mod p on load
     u32 red_wp;        // floor(2^32 / p)
+    int tma;           // prefetch operand rows with cp.async.bulk (1 product per CTA,
+                       // 16-byte aligned rows); staging follows the data buffers
+    int za16, zb16;    // words of a / b rows covered by the bulk copies (multiple of 4)
 };
 
 // 32-bank conflict-free swizzle for the three access patterns used here:
@@ -378,7 +382,25 @@ conv_small_kernel(const ConvSmallParams P) {
     const int t = threadIdx.x % T;
     u32 *bufA = data + grp * 2 * L;
     u32 *bufB = bufA + L;
+    // TMA staging (PPC == 1 only): [mbarrier (16 B)][a row][b row]
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(data + C::PPC * 2 * L);
+    u32 *stA = reinterpret_cast<u32 *>(mbar + 2);
+    u32 *stB = stA + P.za16;
+    const bool tma = C::PPC == 1 && P.tma;
+    auto prefetch = [&](long long r) {  // thread 0 only
+        const u32 ba = 4u * P.za16, bb = 4u * P.zb16;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(mbar, ba + bb);
+        if (ba) bulk_g2s(stA, P.a + r * P.lda, ba, mbar);
+        if (bb) bulk_g2s(stB, P.b + r * P.ldb, bb, mbar);
+    };
+    if (tma && threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        fence_mbar_init();
+    }
     __syncthreads();
+    if (tma && threadIdx.x == 0 && (long long)blockIdx.x < P.batch) prefetch(blockIdx.x);
+    uint32_t phase = 0;
 
     for (long long base = (long long)blockIdx.x * C::PPC; base < P.batch;
          base += (long long)gridDim.x * C::PPC) {
@@ -387,11 +409,25 @@ conv_small_kernel(const ConvSmallParams P) {
         u32 va[16], vb[16];
         const u32 *ga = P.a + (valid ? row : 0) * P.lda;
         const u32 *gb = P.b + (valid ? row : 0) * P.ldb;
+        if (tma) {
+            mbar_wait(mbar, phase);
+            phase ^= 1;
 #pragma unroll
-        for (int s = 0; s < 16; ++s) {
-            const int x = (s << (K - 4)) | t;
-            va[s] = (valid && x < P.z1) ? __ldcs(ga + x) : 0u;
-            vb[s] = (valid && x < P.z2) ? __ldcs(gb + x) : 0u;
+            for (int s = 0; s < 16; ++s) {
+                const int x = (s << (K - 4)) | t;
+                va[s] = x < P.za16 ? stA[x] : (x < P.z1 ? __ldcs(ga + x) : 0u);
+                vb[s] = x < P.zb16 ? stB[x] : (x < P.z2 ? __ldcs(gb + x) : 0u);
+            }
+            __syncthreads();  // staging consumed: refill it for the next product
+            const long long nxt = base + (long long)gridDim.x * C::PPC;
+            if (threadIdx.x == 0 && nxt < P.batch) prefetch(nxt);
+        } else {
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const int x = (s << (K - 4)) | t;
+                va[s] = (valid && x < P.z1) ? __ldcs(ga + x) : 0u;
+                vb[s] = (valid && x < P.z2) ? __ldcs(gb + x) : 0u;
+            }
         }
         if (P.reduce) {  // three-primes inputs: any 32-bit word -> residue
 #pragma unroll
