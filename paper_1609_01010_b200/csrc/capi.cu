@@ -74,6 +74,8 @@ static ConvSmallParams make_params(const FieldTables *T, const u32 *a, long long
     P.linv_mont = T->linv_mont;
     P.tf = T->tf;
     P.ti = T->ti;
+    memcpy(P.c16f, T->h16f, sizeof(P.c16f));
+    memcpy(P.c16i, T->h16i, sizeof(P.c16i));
     const int K = T->log2L;
     if (K >= 4) {
         const u64 G = 1ull << (K - 4);

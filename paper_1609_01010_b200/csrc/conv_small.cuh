@@ -58,6 +58,8 @@ struct ConvSmallParams {
     int tma;           // prefetch operand rows with cp.async.bulk (1 product per CTA,
                        // 16-byte aligned rows); staging follows the data buffers
     int za16, zb16;    // words of a / b rows covered by the bulk copies (multiple of 4)
+    uint2 c16f[16];    // tf[1..15] / ti[1..15]: the thread-invariant twiddles of the
+    uint2 c16i[16];    // lowest pass (h <= 8), read from the constant bank
 };
 
 // 32-bank conflict-free swizzle for the three access patterns used here:
@@ -150,6 +152,19 @@ __device__ __forceinline__ void fwd_lower(u32 (&v)[16], int t, const ConvSmallPa
 #pragma unroll
         for (int s = 0; s < 16; ++s) {
             if ((s >> sbit) & 1) continue;
+            if (SB == 0) {  // twiddle index is compile-time: w_{2h}^(s mod h)
+                const int j = s & (h - 1);
+                if (j == 0) {  // w = 1: no multiplication
+                    u32 &a = v[s], &b = v[s | (1 << sbit)];
+                    const u32 x = a;
+                    a = add_mod(x, b, p);
+                    b = sub_mod(x, b, p);
+                } else {
+                    const uint2 w = P.c16f[h + j];
+                    bfly_dif(v[s], v[s | (1 << sbit)], w.x, w.y, p);
+                }
+                continue;
+            }
             const int j = (tpos | (s << SB)) & (h - 1);
             const uint2 w = ldtw(W.tf, h + j);
             bfly_dif(v[s], v[s | (1 << sbit)], w.x, w.y, p);
@@ -169,6 +184,19 @@ __device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallPa
 #pragma unroll
         for (int s = 0; s < 16; ++s) {
             if ((s >> sbit) & 1) continue;
+            if (SB == 0) {
+                const int j = s & (h - 1);
+                if (j == 0) {  // w = 1
+                    u32 &a = v[s], &b = v[s | (1 << sbit)];
+                    const u32 x = a;
+                    a = add_mod(x, b, p);
+                    b = sub_mod(x, b, p);
+                } else {
+                    const uint2 w = P.c16i[h + j];
+                    bfly_dit(v[s], v[s | (1 << sbit)], w.x, w.y, p);
+                }
+                continue;
+            }
             const int j = (tpos | (s << SB)) & (h - 1);
             const uint2 w = ldtw(W.ti, h + j);
             bfly_dit(v[s], v[s | (1 << sbit)], w.x, w.y, p);

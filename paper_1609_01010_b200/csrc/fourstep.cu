@@ -396,6 +396,10 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     memset(&P, 0, sizeof(P));
     if ((s = get_twist(TL, &P.tw)) != MC_OK) return s;
     P.cs.p = p;
+    // tf[h + j] = w_{2h}^j does not depend on L: the lowest-pass constants of
+    // the column and row transforms are the same
+    memcpy(P.cs.c16f, TR->h16f, sizeof(P.cs.c16f));
+    memcpy(P.cs.c16i, TR->h16i, sizeof(P.cs.c16i));
     P.cs.pinv = TL->pinv;
     P.cs.linv_mont = TL->linv_mont;  // 1/L for the whole transform
     P.a = a;

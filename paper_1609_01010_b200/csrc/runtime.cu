@@ -196,6 +196,10 @@ mc_status get_tables(u32 p, int log2L, const FieldTables **out) {
             acci = mulmod(acci, wi, p);
         }
     }
+    for (u64 i = 0; i < 16 && i < hf.size(); ++i) {
+        T->h16f[i] = hf[i];
+        T->h16i[i] = hi[i];
+    }
     size_t bytes = sizeof(uint2) * hf.size();
     cudaError_t e = cudaMalloc(&T->tf, bytes);
     if (e == cudaSuccess) e = cudaMalloc(&T->ti, bytes);

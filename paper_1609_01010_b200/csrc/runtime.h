@@ -49,6 +49,8 @@ struct FieldTables {
     Shoup linv_mont;    // L^-1 * 2^32 mod p (undoes REDC's 2^-32)
     uint2 *tf = nullptr;
     uint2 *ti = nullptr;
+    uint2 h16f[16] = {};  // host copies of tf[0..15] / ti[0..15]
+    uint2 h16i[16] = {};
 };
 
 // Stage tables (tf/ti) are only materialised up to this size; larger
