@@ -441,10 +441,18 @@ conv_small_kernel(const ConvSmallParams P) {
             mbar_wait(mbar, phase);
             phase ^= 1;
 #pragma unroll
-            for (int s = 0; s < 16; ++s) {
+            for (int s = 0; s < 16; ++s) {  // predicated LDS, no branches
                 const int x = (s << (K - 4)) | t;
-                va[s] = x < P.za16 ? stA[x] : (x < P.z1 ? __ldcs(ga + x) : 0u);
-                vb[s] = x < P.zb16 ? stB[x] : (x < P.z2 ? __ldcs(gb + x) : 0u);
+                va[s] = x < P.za16 ? stA[x] : 0u;
+                vb[s] = x < P.zb16 ? stB[x] : 0u;
+            }
+            if (P.z1 != P.za16 || P.z2 != P.zb16) {  // uniform: rows not a multiple of 4
+#pragma unroll
+                for (int s = 0; s < 16; ++s) {
+                    const int x = (s << (K - 4)) | t;
+                    if (x >= P.za16 && x < P.z1) va[s] = __ldcs(ga + x);
+                    if (x >= P.zb16 && x < P.z2) vb[s] = __ldcs(gb + x);
+                }
             }
             __syncthreads();  // staging consumed: refill it for the next product
             const long long nxt = base + (long long)gridDim.x * C::PPC;
