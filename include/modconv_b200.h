@@ -142,6 +142,19 @@ mc_status mc_conv_host(int engine, const uint32_t *a, int64_t lda, int32_t z1,
                        const uint32_t *b, int64_t ldb, int32_t z2, uint32_t *c,
                        int64_t ldc, int64_t batch, uint32_t p);
 
+/* Host-buffer batched call, asynchronous and pipelined: the batch is cut
+ * into chunks of `chunk_rows` products (0 = automatic); for each chunk the
+ * H2D copy of its operand rows, the convolution kernel and the D2H copy of
+ * its products run on three internal streams, so copies in both directions
+ * overlap each other and the kernels.  The call is ordered after prior work
+ * on `stream` and `stream` waits for the last D2H before later work.  Host
+ * buffers should be pinned (cudaHostAlloc) for the copies to overlap.  The
+ * caller must not touch c before synchronizing `stream`. */
+mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t z1,
+                             const uint32_t *b, int64_t ldb, int32_t z2, uint32_t *c,
+                             int64_t ldc, int64_t batch, uint32_t p, int64_t chunk_rows,
+                             void *stream);
+
 /* Seeded input generator (splitmix64, see oracle/modconv_oracle.c):
  * out[r*ld + i] = gen(seed, stream, row0 + r, i) mod-scaled to [0, hi). */
 mc_status mc_gen_u32(uint64_t seed, uint64_t stream_id, uint64_t row0,

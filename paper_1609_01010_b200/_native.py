@@ -43,6 +43,8 @@ _SIGS = {
     "mc_mul_mod_prime_k": ([vp, i32, vp, i32, vp, ctypes.c_int, vp], ctypes.c_int),
     "mc_conv_host": ([ctypes.c_int, vp, i64, i32, vp, i64, i32, vp, i64, i64, u32],
                      ctypes.c_int),
+    "mc_conv_host_async": ([ctypes.c_int, vp, i64, i32, vp, i64, i32, vp, i64, i64, u32, i64,
+                            vp], ctypes.c_int),
     "mc_gen_u32": ([u64, u64, u64, i64, i64, u64, vp, i64, vp], ctypes.c_int),
     "mc_ubench_int_pipes": ([ctypes.POINTER(ctypes.c_double), ctypes.c_int,
                              ctypes.POINTER(ctypes.c_double)], ctypes.c_int),

@@ -52,7 +52,8 @@ def _deps_mtime():
 
 def _compile(unit, verbose):
     src, obj, extra = unit
-    cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", src, "-o", obj]
+    cmd = [NVCC, *ARCH, *FLAGS, *extra, *os.environ.get("MC_EXTRA_FLAGS", "").split(), "-c",
+           src, "-o", obj]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
     r = subprocess.run(cmd, capture_output=True, text=True)

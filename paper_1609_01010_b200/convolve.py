@@ -106,28 +106,45 @@ def conv_batch(a: torch.Tensor, b: torch.Tensor, field, engine: str = "tft",
     if host != (b.device.type == "cpu"):
         raise ValueError("a and b must be on the same device")
     if host:
-        a_d = a.to(dev, non_blocking=True)
-        b_d = b.to(dev, non_blocking=True)
-    else:
-        a_d, b_d = a, b
+        return _conv_batch_host(a, b, fp, engine, out, counters, stream)
+    a_d, b_d = a, b
     if a_d.stride(1) != 1 or b_d.stride(1) != 1:
         a_d, b_d = a_d.contiguous(), b_d.contiguous()
-    if out is not None and not host:
+    if out is not None:
         c_d = _tensors.as_words(out)
-        if c_d.shape != (B, n) or c_d.stride(1) != 1:
-            raise ValueError(f"out must be [B, {n}] with unit column stride")
+        if c_d.shape != (B, n) or c_d.stride(1) != 1 or c_d.device != a_d.device:
+            raise ValueError(f"out must be a [B, {n}] tensor on {a_d.device} with unit column stride")
     else:
-        c_d = torch.empty((B, n), dtype=torch.int32, device=dev)
+        c_d = torch.empty((B, n), dtype=torch.int32, device=a_d.device)
     fn = _native.lib().mc_conv_tft if engine == "tft" else _native.lib().mc_conv_fft_pad
     _native.check(fn(_tensors.ptr(a_d), a_d.stride(0), z1, _tensors.ptr(b_d), b_d.stride(0), z2,
                      _tensors.ptr(c_d), c_d.stride(0), B, fp.p, _tensors.stream_handle(stream)))
     count_engine(engine, z1, z2, counters, B)
-    if host:
-        if out is not None:
-            out.copy_(c_d, non_blocking=True)
-            return out
-        return c_d.to("cpu")
     return c_d
+
+
+def _conv_batch_host(a, b, fp, engine, out, counters, stream) -> torch.Tensor:
+    """Host tensors: chunked H2D / kernel / D2H pipeline on three streams
+    (mc_conv_host_async).  Pinned buffers overlap copies in both directions
+    with the kernels.  The result is complete when the call returns."""
+    B, z1 = a.shape
+    z2 = b.shape[1]
+    n = z1 + z2 - 1
+    a_h = a if a.stride(1) == 1 else a.contiguous()
+    b_h = b if b.stride(1) == 1 else b.contiguous()
+    if out is not None:
+        c_h = _tensors.as_words(out)
+        if c_h.shape != (B, n) or c_h.stride(1) != 1 or c_h.device.type != "cpu":
+            raise ValueError(f"out must be a CPU [B, {n}] tensor with unit column stride")
+    else:
+        c_h = torch.empty((B, n), dtype=torch.int32, pin_memory=a_h.is_pinned())
+    st = stream if stream is not None else torch.cuda.current_stream()
+    _native.check(_native.lib().mc_conv_host_async(
+        1 if engine == "tft" else 0, _tensors.ptr(a_h), a_h.stride(0), z1, _tensors.ptr(b_h),
+        b_h.stride(0), z2, _tensors.ptr(c_h), c_h.stride(0), B, fp.p, 0, int(st.cuda_stream)))
+    st.synchronize()
+    count_engine(engine, z1, z2, counters, B)
+    return out if out is not None else c_h
 
 
 # ------------------------------------------------------------------ list API

@@ -234,6 +234,109 @@ mc_status mc_conv_host(int engine, const uint32_t *a, int64_t lda, int32_t z1,
     return MC_OK;
 }
 
+// ---------------------------------------------------------------- pipelined host call
+struct PipeState {
+    int dev = -1;
+    cudaStream_t s_in = nullptr, s_cmp = nullptr, s_out = nullptr;
+    static constexpr int NBUF = 3;
+    cudaEvent_t ev_in[NBUF] = {}, ev_cmp[NBUF] = {}, ev_out[NBUF] = {}, ev_start = nullptr;
+    void *buf = nullptr;
+    size_t bytes = 0;
+};
+
+static std::mutex g_pipe_mu;
+
+mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t z1,
+                             const uint32_t *b, int64_t ldb, int32_t z2, uint32_t *c,
+                             int64_t ldc, int64_t batch, uint32_t p, int64_t chunk_rows,
+                             void *stream) {
+    static thread_local PipeState S;
+    if (engine != 0 && engine != 1) return fail(MC_EINVAL, "engine must be 0 (fft_pad) or 1 (tft)");
+    if (z1 < 1 || z2 < 1) return fail(MC_EINVAL, "inputs must be nonempty");
+    const int64_t n = (int64_t)z1 + z2 - 1;
+    if (lda < z1 || ldb < z2 || ldc < n) return fail(MC_EINVAL, "bad leading dimension");
+    if (batch <= 0) return batch == 0 ? MC_OK : fail(MC_EINVAL, "negative batch");
+    if (!a || !b || !c) return fail(MC_EINVAL, "null pointer");
+    {  // validate the field / size up front (synchronous errors, nothing launched)
+        int K = 0;
+        while ((1ll << K) < n) ++K;
+        const FieldTables *T;
+        mc_status st = get_tables(p, K, &T);
+        if (st != MC_OK) return st;
+    }
+    cudaStream_t user = (cudaStream_t)stream;
+    const int dev = current_device();
+    if (S.dev != dev) {
+        std::lock_guard<std::mutex> lock(g_pipe_mu);
+        MC_CUDA_CHECK(cudaStreamCreateWithFlags(&S.s_in, cudaStreamNonBlocking));
+        MC_CUDA_CHECK(cudaStreamCreateWithFlags(&S.s_cmp, cudaStreamNonBlocking));
+        MC_CUDA_CHECK(cudaStreamCreateWithFlags(&S.s_out, cudaStreamNonBlocking));
+        for (int k = 0; k < PipeState::NBUF; ++k) {
+            MC_CUDA_CHECK(cudaEventCreateWithFlags(&S.ev_in[k], cudaEventDisableTiming));
+            MC_CUDA_CHECK(cudaEventCreateWithFlags(&S.ev_cmp[k], cudaEventDisableTiming));
+            MC_CUDA_CHECK(cudaEventCreateWithFlags(&S.ev_out[k], cudaEventDisableTiming));
+        }
+        MC_CUDA_CHECK(cudaEventCreateWithFlags(&S.ev_start, cudaEventDisableTiming));
+        S.dev = dev;
+        S.buf = nullptr;
+        S.bytes = 0;
+    }
+    if (chunk_rows <= 0) {  // ~8 chunks, at least 64 rows, at most ~16 MiB of operands
+        chunk_rows = std::max<int64_t>(64, (batch + 7) / 8);
+        const int64_t cap = std::max<int64_t>(1, (16ll << 20) / (4 * (z1 + z2 + n)));
+        chunk_rows = std::min(chunk_rows, std::max<int64_t>(cap, 1));
+    }
+    chunk_rows = std::min(chunk_rows, batch);
+    const size_t per_buf = 4ull * chunk_rows * (z1 + z2 + n);
+    if (S.bytes < per_buf * PipeState::NBUF) {
+        MC_CUDA_CHECK(cudaStreamSynchronize(S.s_out));
+        if (S.buf) cudaFree(S.buf);
+        S.buf = nullptr;
+        MC_CUDA_CHECK(cudaMalloc(&S.buf, per_buf * PipeState::NBUF));
+        S.bytes = per_buf * PipeState::NBUF;
+    }
+    MC_CUDA_CHECK(cudaEventRecord(S.ev_start, user));
+    MC_CUDA_CHECK(cudaStreamWaitEvent(S.s_in, S.ev_start, 0));
+    const int64_t nch = (batch + chunk_rows - 1) / chunk_rows;
+    for (int64_t i = 0; i < nch; ++i) {
+        const int k = (int)(i % PipeState::NBUF);
+        const int64_t r0 = i * chunk_rows, rows = std::min(chunk_rows, batch - r0);
+        uint32_t *da = (uint32_t *)((char *)S.buf + per_buf * k);
+        uint32_t *db = da + chunk_rows * z1;
+        uint32_t *dc = db + chunk_rows * z2;
+        if (i >= PipeState::NBUF) MC_CUDA_CHECK(cudaStreamWaitEvent(S.s_in, S.ev_out[k], 0));
+        if (lda == z1)  // contiguous rows: one linear DMA per operand chunk
+            MC_CUDA_CHECK(cudaMemcpyAsync(da, a + r0 * lda, 4ull * z1 * rows,
+                                          cudaMemcpyHostToDevice, S.s_in));
+        else
+            MC_CUDA_CHECK(cudaMemcpy2DAsync(da, 4 * z1, a + r0 * lda, 4 * lda, 4 * z1, rows,
+                                            cudaMemcpyHostToDevice, S.s_in));
+        if (ldb == z2)
+            MC_CUDA_CHECK(cudaMemcpyAsync(db, b + r0 * ldb, 4ull * z2 * rows,
+                                          cudaMemcpyHostToDevice, S.s_in));
+        else
+            MC_CUDA_CHECK(cudaMemcpy2DAsync(db, 4 * z2, b + r0 * ldb, 4 * ldb, 4 * z2, rows,
+                                            cudaMemcpyHostToDevice, S.s_in));
+        MC_CUDA_CHECK(cudaEventRecord(S.ev_in[k], S.s_in));
+        MC_CUDA_CHECK(cudaStreamWaitEvent(S.s_cmp, S.ev_in[k], 0));
+        mc_status st = conv_dispatch(engine, da, z1, z1, db, z2, z2, dc, n, rows, p, S.s_cmp);
+        if (st != MC_OK) return st;
+        MC_CUDA_CHECK(cudaEventRecord(S.ev_cmp[k], S.s_cmp));
+        MC_CUDA_CHECK(cudaStreamWaitEvent(S.s_out, S.ev_cmp[k], 0));
+        if (ldc == n)
+            MC_CUDA_CHECK(cudaMemcpyAsync(c + r0 * ldc, dc, 4ull * n * rows,
+                                          cudaMemcpyDeviceToHost, S.s_out));
+        else
+            MC_CUDA_CHECK(cudaMemcpy2DAsync(c + r0 * ldc, 4 * ldc, dc, 4 * n, 4 * n, rows,
+                                            cudaMemcpyDeviceToHost, S.s_out));
+        MC_CUDA_CHECK(cudaEventRecord(S.ev_out[k], S.s_out));
+    }
+    // the user's stream continues after the last D2H
+    const int last = (int)((nch - 1) % PipeState::NBUF);
+    MC_CUDA_CHECK(cudaStreamWaitEvent(user, S.ev_out[last], 0));
+    return MC_OK;
+}
+
 // ---------------------------------------------------------------- generator
 __device__ __forceinline__ unsigned long long sm64(unsigned long long x) {
     unsigned long long z = x + 0x9E3779B97F4A7C15ull;
