@@ -76,16 +76,8 @@ static ConvSmallParams make_params(const FieldTables *T, const u32 *a, long long
     P.ti = T->ti;
     memcpy(P.c16f, T->h16f, sizeof(P.c16f));
     memcpy(P.c16i, T->h16i, sizeof(P.c16i));
-    const int K = T->log2L;
-    if (K >= 4) {
-        const u64 G = 1ull << (K - 4);
-        for (int l = 1; l <= 4; ++l) {
-            u64 m = (G << l) % T->p;
-            u64 h = (G << (l - 1)) % T->p;
-            P.mlev[l] = shoup((u32)m, T->p);
-            P.hinv[l] = shoup(inv_mod((u32)h, T->p), T->p);
-        }
-    }
+    memcpy(P.mlev, T->mlev, sizeof(P.mlev));
+    memcpy(P.hinv, T->hinv, sizeof(P.hinv));
     return P;
 }
 

@@ -101,6 +101,7 @@ mc_status mc_mul_three_primes(const uint32_t *a, int32_t z1, const uint32_t *b, 
     uint32_t *res = scratch;
     bool own = false;
     if (!res) {
+        keep_pool_memory();
         MC_CUDA_CHECK(cudaMallocAsync(&res, sizeof(uint32_t) * 3 * n, st));
         own = true;
     }

@@ -421,6 +421,7 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     const long long budget_words = 16ll << 20;  // 64 MiB of scratch: stays L2-resident
     const long long chunk = std::max(1ll, std::min(batch, budget_words / (2 * L)));
     u32 *scratch = nullptr;
+    keep_pool_memory();
     MC_CUDA_CHECK(cudaMallocAsync(&scratch, sizeof(u32) * 2 * L * chunk, st));
     P.Ah = scratch;
     P.Bh = scratch + L * chunk;

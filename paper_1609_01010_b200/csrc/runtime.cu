@@ -142,6 +142,20 @@ int current_device() {
     return d;
 }
 
+// Keep stream-ordered scratch (cudaMallocAsync) in the device's default pool
+// across synchronizations instead of unmapping it each time.
+void keep_pool_memory() {
+    static bool done[64] = {false};
+    const int d = current_device();
+    if (d < 64 && done[d]) return;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+        unsigned long long thr = ~0ull;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    if (d < 64) done[d] = true;
+}
+
 int sm_count() {
     static int cached[64] = {0};
     int d = current_device();
@@ -176,6 +190,13 @@ mc_status get_tables(u32 p, int log2L, const FieldTables **out) {
     u32 li = inv_mod((u32)(L % p), p);
     T->linv = shoup(li, p);
     T->linv_mont = shoup((u32)mulmod(li, (1ull << 32) % p, p), p);
+    if (log2L >= 4) {  // level constants of the fused kernel's top pass
+        const u64 G = 1ull << (log2L - 4);
+        for (int l = 1; l <= 4; ++l) {
+            T->mlev[l] = shoup((u32)((G << l) % p), p);
+            T->hinv[l] = shoup(inv_mod((u32)((G << (l - 1)) % p), p), p);
+        }
+    }
     if (log2L > kMaxStageTableLog2) {  // large L: four-step sub-tables only
         g_tabs[key] = T;
         *out = T;

@@ -51,6 +51,8 @@ struct FieldTables {
     uint2 *ti = nullptr;
     uint2 h16f[16] = {};  // host copies of tf[0..15] / ti[0..15]
     uint2 h16i[16] = {};
+    Shoup mlev[5] = {};   // fused-kernel top-level constants (see ConvSmallParams)
+    Shoup hinv[5] = {};
 };
 
 // Stage tables (tf/ti) are only materialised up to this size; larger
@@ -62,6 +64,7 @@ constexpr int kMaxStageTableLog2 = 16;
 mc_status get_tables(u32 p, int log2L, const FieldTables **out);
 
 int current_device();
+void keep_pool_memory();
 int sm_count();
 
 }  // namespace mc

@@ -238,6 +238,7 @@ mc_status mc_ntt(const uint32_t *x, uint32_t *y, int32_t log2L, int64_t batch, u
     cudaStream_t st = (cudaStream_t)stream;
     const long long L = 1ll << log2L;
     u32 *w = nullptr;
+    keep_pool_memory();
     MC_CUDA_CHECK(cudaMallocAsync(&w, 4ull * L * batch, st));
     P.w = w;
     P.ldw = L;
@@ -270,6 +271,7 @@ mc_status mc_tft(const uint32_t *x, int32_t z, uint32_t *y, int32_t n, int32_t l
     if (!x || !y) return fail(MC_EINVAL, "null pointer");
     cudaStream_t st = (cudaStream_t)stream;
     u32 *w = nullptr;
+    keep_pool_memory();
     MC_CUDA_CHECK(cudaMallocAsync(&w, 4ull * L * batch, st));
     P.w = w;
     P.ldw = L;
@@ -304,6 +306,7 @@ mc_status mc_itft(const uint32_t *xhat, uint32_t *y, int32_t n, int32_t log2L, i
     if (!xhat || !y) return fail(MC_EINVAL, "null pointer");
     cudaStream_t st = (cudaStream_t)stream;
     u32 *w = nullptr;
+    keep_pool_memory();
     MC_CUDA_CHECK(cudaMallocAsync(&w, 4ull * L * batch, st));
     P.w = w;
     P.ldw = L;
