@@ -124,11 +124,18 @@ __device__ __forceinline__ void fwd_top_zs(u32 (&v)[16], int t, const ConvSmallP
     }
 }
 
+// Granularity of the compile-time zero-pruning variants (in top slots):
+// finer = more pruning, larger code (instruction-cache pressure).
+#ifndef MC_ZS_STEP
+#define MC_ZS_STEP 4
+#endif
+
 template <int K, int NT>
 __device__ __forceinline__ void fwd_top(u32 (&v)[16], int z, int t, const ConvSmallParams &P,
                                         const Tw &W) {
     constexpr int G = 1 << (K - 4);
     const int zs = (z + G - 1) / G;  // uniform across the launch
+#if MC_ZS_STEP == 2
     if (zs <= 2) fwd_top_zs<K, NT, 2>(v, t, P, W);
     else if (zs <= 4) fwd_top_zs<K, NT, 4>(v, t, P, W);
     else if (zs <= 6) fwd_top_zs<K, NT, 6>(v, t, P, W);
@@ -137,6 +144,15 @@ __device__ __forceinline__ void fwd_top(u32 (&v)[16], int z, int t, const ConvSm
     else if (zs <= 12) fwd_top_zs<K, NT, 12>(v, t, P, W);
     else if (zs <= 14) fwd_top_zs<K, NT, 14>(v, t, P, W);
     else fwd_top_zs<K, NT, 16>(v, t, P, W);
+#elif MC_ZS_STEP == 4
+    if (zs <= 4) fwd_top_zs<K, NT, 4>(v, t, P, W);
+    else if (zs <= 8) fwd_top_zs<K, NT, 8>(v, t, P, W);
+    else if (zs <= 12) fwd_top_zs<K, NT, 12>(v, t, P, W);
+    else fwd_top_zs<K, NT, 16>(v, t, P, W);
+#else
+    if (zs <= 8) fwd_top_zs<K, NT, 8>(v, t, P, W);
+    else fwd_top_zs<K, NT, 16>(v, t, P, W);
+#endif
 }
 
 // ---------------------------------------------------------------- lower passes
