@@ -57,6 +57,15 @@ def _dist():
     return ws, rank, local
 
 
+def _coll_device(dev):
+    """Device for collective tensors: the GPU under NCCL, the host under gloo."""
+    import torch.distributed as dist
+
+    if dist.is_initialized() and dist.get_backend() != "nccl":
+        return "cpu"
+    return dev
+
+
 def _peaks():
     path = os.path.join(REPO, "MEASURED_PEAKS.json")
     try:
@@ -197,8 +206,16 @@ def run_mine(args, cfg):
     if ws > 1:
         import torch.distributed as dist
 
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # BENCH_BACKEND=gloo exercises the multi-rank path on a single GPU
+        # (host-side barriers / reductions only; no rank waits on another's
+        # kernels).  Production runs use NCCL, one GPU per rank.
+        backend = os.environ.get("BENCH_BACKEND", "nccl")
+        ngpu = torch.cuda.device_count()
+        torch.cuda.set_device(local % ngpu)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
     import paper_1609_01010_b200 as mc
@@ -289,7 +306,7 @@ def run_mine(args, cfg):
     clk = clocks.stop()
     times = [s.elapsed_time(e) for s, e in ev]  # ms
     total_ms = sum(times)
-    t_local = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    t_local = torch.tensor([total_ms], dtype=torch.float64, device=_coll_device(dev))
     if ws > 1:
         torch.distributed.all_reduce(t_local, op=torch.distributed.ReduceOp.MAX)
     t_max = float(t_local.item())
@@ -317,7 +334,7 @@ def run_mine(args, cfg):
             ev2[i][1].record(stream)
         barrier()
         t2 = torch.tensor([sum(s.elapsed_time(e) for s, e in ev2)], dtype=torch.float64,
-                          device=dev)
+                          device=_coll_device(dev))
         if ws > 1:
             torch.distributed.all_reduce(t2, op=torch.distributed.ReduceOp.MAX)
         assert torch.equal(c_h.to(dev), c), "e2e output differs from device-resident output"

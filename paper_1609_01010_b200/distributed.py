@@ -79,7 +79,9 @@ def mul_three_primes_distributed(a: torch.Tensor, b: torch.Tensor, dst: int = 0,
     mine = {k: prime_product(a, b, k) for k in primes_of_rank(ws, rank)}
     if ws == 1:
         return crt(mine[0], mine[1], mine[2])
-    # one gather per prime from its owner (ranks >= 3 own nothing)
+    # one gather per prime from its owner (ranks >= 3 own nothing); under a
+    # host backend (gloo) device tensors travel through host memory
+    host_coll = dist.get_backend(group) != "nccl" and a.device.type == "cuda"
     residues = {}
     for k in range(3):
         owner = k % ws
@@ -88,11 +90,12 @@ def mul_three_primes_distributed(a: torch.Tensor, b: torch.Tensor, dst: int = 0,
                 residues[k] = mine[k]
             continue
         if rank == owner:
-            dist.send(mine[k].contiguous(), dst=dst, group=group)
+            t = mine[k].contiguous()
+            dist.send(t.cpu() if host_coll else t, dst=dst, group=group)
         elif rank == dst:
-            buf = torch.empty(n, dtype=torch.int32, device=a.device)
+            buf = torch.empty(n, dtype=torch.int32, device="cpu" if host_coll else a.device)
             dist.recv(buf, src=owner, group=group)
-            residues[k] = buf
+            residues[k] = buf.to(a.device) if host_coll else buf
     if rank != dst:
         return None
     return crt(residues[0], residues[1], residues[2])
