@@ -98,6 +98,20 @@ mc_status mc_mul_three_primes(const uint32_t *a, int32_t z1, const uint32_t *b, 
     if (!a || !b || !limbs) return fail(MC_EINVAL, "null pointer");
     const long long n = (long long)z1 + z2 - 1;
     cudaStream_t st = (cudaStream_t)stream;
+    // The three prime channels are independent: fork them onto three streams
+    // so their kernels fill the GPU together, join for the CRT.
+    static thread_local int dev_cached = -1;
+    static thread_local cudaStream_t fs[3];
+    static thread_local cudaEvent_t fork_ev, done_ev[3];
+    const int dev = current_device();
+    if (dev_cached != dev) {
+        for (int k = 0; k < 3; ++k) {
+            MC_CUDA_CHECK(cudaStreamCreateWithFlags(&fs[k], cudaStreamNonBlocking));
+            MC_CUDA_CHECK(cudaEventCreateWithFlags(&done_ev[k], cudaEventDisableTiming));
+        }
+        MC_CUDA_CHECK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+        dev_cached = dev;
+    }
     uint32_t *res = scratch;
     bool own = false;
     if (!res) {
@@ -105,9 +119,14 @@ mc_status mc_mul_three_primes(const uint32_t *a, int32_t z1, const uint32_t *b, 
         MC_CUDA_CHECK(cudaMallocAsync(&res, sizeof(uint32_t) * 3 * n, st));
         own = true;
     }
+    MC_CUDA_CHECK(cudaEventRecord(fork_ev, st));
     mc_status s = MC_OK;
-    for (int k = 0; k < 3 && s == MC_OK; ++k)
-        s = conv_dispatch_reduced(a, z1, b, z2, res + k * n, kP[k], st);
+    for (int k = 0; k < 3; ++k) {
+        MC_CUDA_CHECK(cudaStreamWaitEvent(fs[k], fork_ev, 0));
+        if (s == MC_OK) s = conv_dispatch_reduced(a, z1, b, z2, res + k * n, kP[k], fs[k]);
+        MC_CUDA_CHECK(cudaEventRecord(done_ev[k], fs[k]));
+        MC_CUDA_CHECK(cudaStreamWaitEvent(st, done_ev[k], 0));
+    }
     if (s == MC_OK) s = launch_crt(res, res + n, res + 2 * n, limbs, n, st);
     if (own) cudaFreeAsync(res, st);
     return s;

@@ -1,4 +1,5 @@
 // Four-step large-transform convolution (see fourstep.cuh for the plan).
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -418,7 +419,12 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     P.row_tf = TC->tf;
     P.row_ti = TC->ti;
     const long long L = 1ll << K;
-    const long long budget_words = 16ll << 20;  // 64 MiB of scratch: stays L2-resident
+    // scratch budget per chunk (default 512 MiB: bigger launches beat L2 residency,
+    // the four-step passes are integer-pipe bound; profiles/r01/README.md)
+    static const long long budget_words = [] {
+        const char *e = getenv("MC_FOURSTEP_SCRATCH_MB");
+        return (e ? atoll(e) : 512ll) << 18;  // MiB -> 32-bit words
+    }();
     const long long chunk = std::max(1ll, std::min(batch, budget_words / (2 * L)));
     u32 *scratch = nullptr;
     keep_pool_memory();
