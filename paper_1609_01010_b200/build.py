@@ -30,6 +30,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-Wall", f"-I{INCLUDE}", f"-I{CSRC}"]
 SMALL_KS = range(4, 14)
+COL_KRS = range(4, 13)
 
 
 def _units():
@@ -39,6 +40,9 @@ def _units():
         if base == "conv_small_inst":
             for k in SMALL_KS:
                 units.append((src, os.path.join(OBJ, f"{base}_k{k}.o"), [f"-DMC_K={k}"]))
+        elif base == "fourstep_cols":
+            for k in COL_KRS:
+                units.append((src, os.path.join(OBJ, f"{base}_kr{k}.o"), [f"-DMC_KR={k}"]))
         else:
             units.append((src, os.path.join(OBJ, base + ".o"), []))
     return units

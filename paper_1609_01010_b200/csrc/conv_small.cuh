@@ -355,7 +355,7 @@ __device__ __forceinline__ void inv_lower_chain(u32 *buf, u32 (&v)[16], int t,
 
 // One operand, arbitrary layout: forward lower passes; on exit the slots
 // are in the last lower pass's layout.
-template <int K, int I, class Lay>
+template <int K, int I, class Lay, int NT = 16>
 __device__ __forceinline__ void fwd_lower_chain1(u32 *buf, u32 (&v)[16], int t,
                                                  const ConvSmallParams &P, const Tw &W, Lay lay) {
     if constexpr (I < Plan<K>::NP) {
@@ -365,23 +365,25 @@ __device__ __forceinline__ void fwd_lower_chain1(u32 *buf, u32 (&v)[16], int t,
         put<SBprev>(buf, v, t, lay);
         __syncthreads();
         get<SB>(buf, v, t, lay);
-        fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(v, t, P, W);
-        fwd_lower_chain1<K, I + 1, Lay>(buf, v, t, P, W, lay);
+        if (NT >= 16 || gblock_of_pass<K, I>(t) < NT)
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(v, t, P, W);
+        fwd_lower_chain1<K, I + 1, Lay, NT>(buf, v, t, P, W, lay);
     }
 }
 
-template <int K, int I, class Lay>
+template <int K, int I, class Lay, int NT = 16>
 __device__ __forceinline__ void inv_lower_chain1(u32 *buf, u32 (&v)[16], int t,
                                                  const ConvSmallParams &P, const Tw &W, Lay lay) {
     if constexpr (I >= 0) {
         constexpr int SB = Plan<K>::sb(I);
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
-        inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(v, t, P, W);
+        if (NT >= 16 || gblock_of_pass<K, I>(t) < NT)
+            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(v, t, P, W);
         __syncthreads();
         put<SB>(buf, v, t, lay);
         __syncthreads();
         get<SBnext>(buf, v, t, lay);
-        inv_lower_chain1<K, I - 1, Lay>(buf, v, t, P, W, lay);
+        inv_lower_chain1<K, I - 1, Lay, NT>(buf, v, t, P, W, lay);
     }
 }
 

@@ -5,132 +5,9 @@
 #include <tuple>
 #include <vector>
 
-#include "conv_small.cuh"
-#include "fourstep.cuh"
+#include "fourstep_int.cuh"
 
 namespace mc {
-
-// Twiddle powers w_L^e for any e < L: lo[e & 4095] (plain) times hi[e >> 12]
-// (Shoup pair).  Forward (w) and inverse (w^-1) sets.
-struct TwistTabs {
-    const u32 *lo_f;
-    const uint2 *hi_f;
-    const u32 *lo_i;
-    const uint2 *hi_i;
-    double two32_over_p;  // 2^32 / p, for Shoup companions computed on the fly
-};
-
-struct FourParams {
-    ConvSmallParams cs;  // p, pinv, linv_mont (for the full L), level constants
-    const u32 *a;
-    const u32 *b;
-    u32 *c;
-    long long lda, ldb, ldc;
-    long long z1, z2, n;
-    u32 *Ah;  // scratch: [chunk][L] transformed a, later the product spectrum
-    u32 *Bh;  // scratch: [chunk][L] transformed b
-    long long prod0;  // first product of this chunk
-    int chunk;
-    int reduce;  // inputs are arbitrary words: reduce mod p on load
-    u32 red_wp;  // floor(2^32 / p)
-    TwistTabs tw;
-    const uint2 *col_tf, *col_ti;  // stage tables for the R-point column transforms
-    const uint2 *row_tf, *row_ti;  // stage tables for the C-point row transforms
-};
-
-__device__ __forceinline__ u32 pow_w(const u32 *lo, const uint2 *hi, u32 e, u32 p) {
-    const uint2 h = __ldg(hi + (e >> 12));
-    return mul_shoup(__ldg(lo + (e & 4095)), h.x, h.y, p);
-}
-
-// floor(w * 2^32 / p) via a double estimate and one exact correction step.
-__device__ __forceinline__ u32 shoup_comp(u32 w, u32 p, double two32_over_p) {
-    u32 q = __double2uint_rz((double)w * two32_over_p);
-    long long r = (long long)(((unsigned long long)w << 32) - (unsigned long long)q * p);
-    if (r < 0) --q;
-    else if (r >= (long long)p) ++q;
-    return q;
-}
-
-// ---------------------------------------------------------------- column kernels
-template <int KR>
-struct ColCfg {
-    static constexpr int R = 1 << KR;
-    static constexpr int TC = 16384 >> KR;  // columns per tile (tile = 16K words)
-    static constexpr int THREADS = 1024;
-    static constexpr int G = R / 16;
-    static constexpr int SMEM = R * 8 + 16384 * 4;
-};
-
-template <int KR, int KC>
-__global__ void __launch_bounds__(1024, 1) col_fwd_kernel(const FourParams P) {
-    using C = ColCfg<KR>;
-    constexpr long long Ccols = 1ll << KC;
-    extern __shared__ uint4 smem_raw[];
-    uint2 *tf_s = reinterpret_cast<uint2 *>(smem_raw);
-    u32 *tile = reinterpret_cast<u32 *>(tf_s + C::R);
-    for (int i = threadIdx.x; i < C::R / 2; i += C::THREADS)
-        reinterpret_cast<uint4 *>(tf_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_tf) + i);
-    const Tw W{tf_s, tf_s};
-    const int op = blockIdx.y;
-    const long long prod = P.prod0 + blockIdx.z;
-    const u32 *src = op ? P.b + prod * P.ldb : P.a + prod * P.lda;
-    const long long z = op ? P.z2 : P.z1;
-    u32 *dst = (op ? P.Bh : P.Ah) + (long long)blockIdx.z * (Ccols << KR);
-    const int c = threadIdx.x % C::TC;
-    const int t = threadIdx.x / C::TC;
-    const long long col = (long long)blockIdx.x * C::TC + c;
-    const u32 p = P.cs.p;
-    __syncthreads();
-
-    u32 v[16];
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {
-        const long long idx = (long long)(t + C::G * s) * Ccols + col;
-        u32 x = idx < z ? __ldcs(src + idx) : 0u;
-        if (P.reduce) x = mul_shoup(x, 1u, P.red_wp, p);
-        v[s] = x;
-    }
-    const int zrows = (int)((z + Ccols - 1) / Ccols);
-    fwd_top<KR, 16>(v, zrows, t, P.cs, W);
-    LayCol<C::TC> lay{c};
-    fwd_lower_chain1<KR, 0>(tile, v, t, P.cs, W, lay);
-    constexpr int SB = last_sb<KR>();
-#pragma unroll
-    for (int s = 0; s < 16; ++s) dst[(long long)slot_pos<SB>(t, s) * Ccols + col] = v[s];
-}
-
-template <int KR, int KC>
-__global__ void __launch_bounds__(1024, 1) col_inv_kernel(const FourParams P) {
-    using C = ColCfg<KR>;
-    constexpr long long Ccols = 1ll << KC;
-    extern __shared__ uint4 smem_raw[];
-    uint2 *ti_s = reinterpret_cast<uint2 *>(smem_raw);
-    u32 *tile = reinterpret_cast<u32 *>(ti_s + C::R);
-    for (int i = threadIdx.x; i < C::R / 2; i += C::THREADS)
-        reinterpret_cast<uint4 *>(ti_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_ti) + i);
-    const Tw W{ti_s, ti_s};
-    const long long prod = P.prod0 + blockIdx.z;
-    const u32 *src = P.Ah + (long long)blockIdx.z * (Ccols << KR);
-    u32 *dst = P.c + prod * P.ldc;
-    const int c = threadIdx.x % C::TC;
-    const int t = threadIdx.x / C::TC;
-    const long long col = (long long)blockIdx.x * C::TC + c;
-    __syncthreads();
-
-    u32 v[16];
-    constexpr int SB = last_sb<KR>();
-#pragma unroll
-    for (int s = 0; s < 16; ++s) v[s] = src[(long long)slot_pos<SB>(t, s) * Ccols + col];
-    LayCol<C::TC> lay{c};
-    inv_lower_chain1<KR, Plan<KR>::NP - 1>(tile, v, t, P.cs, W, lay);
-    ItftTop<KR, 16, 16, 0>::run(v, t, P.cs, W);
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {
-        const long long idx = (long long)(t + C::G * s) * Ccols + col;
-        if (idx < P.n) __stcs(dst + idx, v[s]);
-    }
-}
 
 // ---------------------------------------------------------------- row kernel
 template <int KC>
@@ -166,15 +43,15 @@ __global__ void __launch_bounds__(RowCfg<KC>::THREADS, 2) row_conv_kernel(const 
     const Tw W{tf_s, ti_s};
     const u32 p = P.cs.p;
     const long long R = 1ll << KR;
-    const long long rows = R * P.chunk;
+    const long long rows = P.nrows * P.chunk;  // truncated: only rows < nrows
     __syncthreads();
 
     for (long long base = (long long)blockIdx.x * RC::PPC; base < rows;
          base += (long long)gridDim.x * RC::PPC) {
         const long long gr = base + grp;
         const bool valid = gr < rows;
-        const long long prod = valid ? gr >> KR : 0;
-        const u32 r = valid ? (u32)(gr & (R - 1)) : 0u;
+        const long long prod = valid ? gr / P.nrows : 0;
+        const u32 r = valid ? (u32)(gr % P.nrows) : 0u;
         const u32 f1 = __brev(r) >> (32 - KR);
         if (t < 32) {  // per-row twist factors beta_s = w^(f1*G*s), and inverses
             const int s = t & 15;
@@ -291,40 +168,6 @@ mc_status get_twist_tables(u32 p, int K, const u32 **lo_f, const uint2 **hi_f, c
     return MC_OK;
 }
 
-template <class KF>
-static cudaError_t prep_kernel(KF kern, int smem, int threads, int *per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-    if (e != cudaSuccess) return e;
-    if (per_sm) {
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, smem);
-        if (*per_sm < 1) *per_sm = 1;
-    }
-    return e;
-}
-
-template <int KR, int KC>
-static cudaError_t launch_cols(const FourParams &P, bool fwd, cudaStream_t st) {
-    using C = ColCfg<KR>;
-    static bool ready_f = false, ready_i = false;
-    dim3 grid((unsigned)((1u << KC) / C::TC), fwd ? 2u : 1u, (unsigned)P.chunk);
-    if (fwd) {
-        if (!ready_f) {
-            cudaError_t e = prep_kernel(col_fwd_kernel<KR, KC>, C::SMEM, C::THREADS, nullptr);
-            if (e != cudaSuccess) return e;
-            ready_f = true;
-        }
-        col_fwd_kernel<KR, KC><<<grid, C::THREADS, C::SMEM, st>>>(P);
-    } else {
-        if (!ready_i) {
-            cudaError_t e = prep_kernel(col_inv_kernel<KR, KC>, C::SMEM, C::THREADS, nullptr);
-            if (e != cudaSuccess) return e;
-            ready_i = true;
-        }
-        col_inv_kernel<KR, KC><<<grid, C::THREADS, C::SMEM, st>>>(P);
-    }
-    return cudaGetLastError();
-}
-
 template <int KC>
 static cudaError_t launch_rows(const FourParams &P, int KR, cudaStream_t st) {
     using RC = RowCfg<KC>;
@@ -333,34 +176,24 @@ static cudaError_t launch_rows(const FourParams &P, int KR, cudaStream_t st) {
         cudaError_t e = prep_kernel(row_conv_kernel<KC>, RC::SMEM, RC::THREADS, &per_sm);
         if (e != cudaSuccess) return e;
     }
-    long long work = ((1ll << KR) * P.chunk + RC::PPC - 1) / RC::PPC;
+    long long work = (P.nrows * P.chunk + RC::PPC - 1) / RC::PPC;
     long long grid = std::min<long long>(work, (long long)per_sm * sm_count());
     row_conv_kernel<KC><<<(unsigned)grid, RC::THREADS, RC::SMEM, st>>>(P, KR);
     return cudaGetLastError();
 }
 
-template <int KC>
-static cudaError_t launch_cols_kc(int KR, const FourParams &P, bool fwd, cudaStream_t st) {
-    switch (KR) {
-        case 4: return launch_cols<4, KC>(P, fwd, st);
-        case 5: return launch_cols<5, KC>(P, fwd, st);
-        case 6: return launch_cols<6, KC>(P, fwd, st);
-        case 7: return launch_cols<7, KC>(P, fwd, st);
-        case 8: return launch_cols<8, KC>(P, fwd, st);
-        case 9: return launch_cols<9, KC>(P, fwd, st);
-        case 10: return launch_cols<10, KC>(P, fwd, st);
-        case 11: return launch_cols<11, KC>(P, fwd, st);
-        case 12: return launch_cols<12, KC>(P, fwd, st);
-        default: return cudaErrorInvalidValue;
-    }
-}
-
-static cudaError_t launch_cols_any(int KC, int KR, const FourParams &P, bool fwd,
+static cudaError_t launch_cols_any(int KC, int KR, int NT, const FourParams &P, bool fwd,
                                    cudaStream_t st) {
-    switch (KC) {
-        case 10: return launch_cols_kc<10>(KR, P, fwd, st);
-        case 11: return launch_cols_kc<11>(KR, P, fwd, st);
-        case 12: return launch_cols_kc<12>(KR, P, fwd, st);
+    switch (KR) {
+        case 4: return launch_cols_kr4(P, KC, NT, fwd, st);
+        case 5: return launch_cols_kr5(P, KC, NT, fwd, st);
+        case 6: return launch_cols_kr6(P, KC, NT, fwd, st);
+        case 7: return launch_cols_kr7(P, KC, NT, fwd, st);
+        case 8: return launch_cols_kr8(P, KC, NT, fwd, st);
+        case 9: return launch_cols_kr9(P, KC, NT, fwd, st);
+        case 10: return launch_cols_kr10(P, KC, NT, fwd, st);
+        case 11: return launch_cols_kr11(P, KC, NT, fwd, st);
+        case 12: return launch_cols_kr12(P, KC, NT, fwd, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -377,7 +210,6 @@ static cudaError_t launch_rows_any(int KC, int KR, const FourParams &P, cudaStre
 mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u32 *b,
                         long long ldb, int z2, u32 *c, long long ldc, long long batch, u32 p,
                         cudaStream_t st, int circ_log2L, bool reduce_inputs) {
-    (void)engine;  // the product is exact either way; large L always pads
     const bool circ = circ_log2L >= 0;
     const long long n = circ ? (1ll << circ_log2L) : (long long)z1 + z2 - 1;
     int K = 0;
@@ -397,6 +229,8 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     memset(&P, 0, sizeof(P));
     if ((s = get_twist(TL, &P.tw)) != MC_OK) return s;
     P.cs.p = p;
+    memcpy(P.cs.mlev, TR->mlev, sizeof(P.cs.mlev));  // column-level ITFT constants
+    memcpy(P.cs.hinv, TR->hinv, sizeof(P.cs.hinv));
     // tf[h + j] = w_{2h}^j does not depend on L: the lowest-pass constants of
     // the column and row transforms are the same
     memcpy(P.cs.c16f, TR->h16f, sizeof(P.cs.c16f));
@@ -419,6 +253,12 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     P.row_tf = TC->tf;
     P.row_ti = TC->ti;
     const long long L = 1ll << K;
+    // Truncation (tft engine): relaxed to L/16 granularity like the fused
+    // kernel; the column transforms are truncated at NT of their 16 top
+    // blocks and the row pass only forms rows < NT * R/16.
+    int NT = 16;
+    if (engine == 1 && !circ) NT = (int)((n + (L >> 4) - 1) / (L >> 4));
+    P.nrows = (long long)NT << (KR - 4);
     // scratch budget per chunk (default 512 MiB: bigger launches beat L2 residency,
     // the four-step passes are integer-pipe bound; profiles/r01/README.md)
     static const long long budget_words = [] {
@@ -435,9 +275,9 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     for (long long p0 = 0; p0 < batch && result == MC_OK; p0 += chunk) {
         P.prod0 = p0;
         P.chunk = (int)std::min(chunk, batch - p0);
-        cudaError_t e = launch_cols_any(KC, KR, P, true, st);
+        cudaError_t e = launch_cols_any(KC, KR, NT, P, true, st);
         if (e == cudaSuccess) e = launch_rows_any(KC, KR, P, st);
-        if (e == cudaSuccess) e = launch_cols_any(KC, KR, P, false, st);
+        if (e == cudaSuccess) e = launch_cols_any(KC, KR, NT, P, false, st);
         note_launches(3);
         if (e != cudaSuccess) result = cuda_fail(e, "four-step launch");
     }

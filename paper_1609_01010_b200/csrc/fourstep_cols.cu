@@ -1,0 +1,154 @@
+// Column passes of the four-step path for one column size KR (compiled once
+// per KR with -DMC_KR=<KR>); see fourstep.cuh for the decomposition.
+#include "fourstep_int.cuh"
+
+#ifndef MC_KR
+#error "compile with -DMC_KR=<log2 R>"
+#endif
+
+namespace mc {
+
+// Forward: R-point DIF down each column of a TC-wide tile.  Truncated (NT <
+// 16): top-pass outputs of blocks >= NT are pruned, lower passes skip those
+// blocks and only rows < NT*R/16 are written.
+template <int KR, int KC, int NT>
+__global__ void __launch_bounds__(1024, 1) col_fwd_kernel(const FourParams P) {
+    using C = ColCfg<KR>;
+    constexpr long long Ccols = 1ll << KC;
+    extern __shared__ uint4 smem_raw[];
+    uint2 *tf_s = reinterpret_cast<uint2 *>(smem_raw);
+    u32 *tile = reinterpret_cast<u32 *>(tf_s + 2 * C::R);
+    for (int i = threadIdx.x; i < C::R / 2; i += C::THREADS)
+        reinterpret_cast<uint4 *>(tf_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_tf) + i);
+    const Tw W{tf_s, tf_s};
+    const int op = blockIdx.y;
+    const long long prod = P.prod0 + blockIdx.z;
+    const u32 *src = op ? P.b + prod * P.ldb : P.a + prod * P.lda;
+    const long long z = op ? P.z2 : P.z1;
+    u32 *dst = (op ? P.Bh : P.Ah) + (long long)blockIdx.z * (Ccols << KR);
+    const int c = threadIdx.x % C::TC;
+    const int t = threadIdx.x / C::TC;
+    const long long col = (long long)blockIdx.x * C::TC + c;
+    const u32 p = P.cs.p;
+    __syncthreads();
+
+    u32 v[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const long long idx = (long long)(t + C::G * s) * Ccols + col;
+        u32 x = idx < z ? __ldcs(src + idx) : 0u;
+        if (P.reduce) x = mul_shoup(x, 1u, P.red_wp, p);
+        v[s] = x;
+    }
+    const int zrows = (int)((z + Ccols - 1) / Ccols);
+    fwd_top<KR, NT>(v, zrows, t, P.cs, W);
+    LayCol<C::TC> lay{c};
+    fwd_lower_chain1<KR, 0, LayCol<C::TC>, NT>(tile, v, t, P.cs, W, lay);
+    constexpr int SB = last_sb<KR>();
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const int row = slot_pos<SB>(t, s);
+        if (NT >= 16 || (row >> (KR - 4)) < NT) dst[(long long)row * Ccols + col] = v[s];
+    }
+}
+
+// Inverse: R-point inverse DIT up each column; truncated (NT < 16): rows
+// >= NT*R/16 hold the column time values, which are zero for a product of
+// length <= NT*L/16, then the van der Hoeven top pass (ItftTop).
+template <int KR, int KC, int NT>
+__global__ void __launch_bounds__(1024, 1) col_inv_kernel(const FourParams P) {
+    using C = ColCfg<KR>;
+    constexpr long long Ccols = 1ll << KC;
+    extern __shared__ uint4 smem_raw[];
+    uint2 *tf_s = reinterpret_cast<uint2 *>(smem_raw);
+    uint2 *ti_s = tf_s + C::R;
+    u32 *tile = reinterpret_cast<u32 *>(tf_s + 2 * C::R);
+    for (int i = threadIdx.x; i < C::R / 2; i += C::THREADS) {
+        reinterpret_cast<uint4 *>(ti_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_ti) + i);
+        if (NT < 16)
+            reinterpret_cast<uint4 *>(tf_s)[i] =
+                __ldg(reinterpret_cast<const uint4 *>(P.col_tf) + i);
+    }
+    const Tw W{tf_s, ti_s};
+    const long long prod = P.prod0 + blockIdx.z;
+    const u32 *src = P.Ah + (long long)blockIdx.z * (Ccols << KR);
+    u32 *dst = P.c + prod * P.ldc;
+    const int c = threadIdx.x % C::TC;
+    const int t = threadIdx.x / C::TC;
+    const long long col = (long long)blockIdx.x * C::TC + c;
+    __syncthreads();
+
+    u32 v[16];
+    constexpr int SB = last_sb<KR>();
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const int row = slot_pos<SB>(t, s);
+        v[s] = (NT >= 16 || (row >> (KR - 4)) < NT) ? src[(long long)row * Ccols + col] : 0u;
+    }
+    LayCol<C::TC> lay{c};
+    inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, NT>(tile, v, t, P.cs, W, lay);
+    ItftTop<KR, 16, NT, 0>::run(v, t, P.cs, W);
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const long long idx = (long long)(t + C::G * s) * Ccols + col;
+        if (idx < P.n) __stcs(dst + idx, v[s]);
+    }
+}
+
+template <int KR, int KC, int NT>
+static cudaError_t launch_one(const FourParams &P, bool fwd, cudaStream_t st) {
+    using C = ColCfg<KR>;
+    static bool ready_f = false, ready_i = false;  // benign races: idempotent
+    dim3 grid((unsigned)((1u << KC) / C::TC), fwd ? 2u : 1u, (unsigned)P.chunk);
+    if (fwd) {
+        if (!ready_f) {
+            cudaError_t e = prep_kernel(col_fwd_kernel<KR, KC, NT>, C::SMEM, C::THREADS, nullptr);
+            if (e != cudaSuccess) return e;
+            ready_f = true;
+        }
+        col_fwd_kernel<KR, KC, NT><<<grid, C::THREADS, C::SMEM, st>>>(P);
+    } else {
+        if (!ready_i) {
+            cudaError_t e = prep_kernel(col_inv_kernel<KR, KC, NT>, C::SMEM, C::THREADS, nullptr);
+            if (e != cudaSuccess) return e;
+            ready_i = true;
+        }
+        col_inv_kernel<KR, KC, NT><<<grid, C::THREADS, C::SMEM, st>>>(P);
+    }
+    return cudaGetLastError();
+}
+
+template <int KR, int KC>
+static cudaError_t launch_nt(const FourParams &P, int NT, bool fwd, cudaStream_t st) {
+    switch (NT) {
+        case 9: return launch_one<KR, KC, 9>(P, fwd, st);
+        case 10: return launch_one<KR, KC, 10>(P, fwd, st);
+        case 11: return launch_one<KR, KC, 11>(P, fwd, st);
+        case 12: return launch_one<KR, KC, 12>(P, fwd, st);
+        case 13: return launch_one<KR, KC, 13>(P, fwd, st);
+        case 14: return launch_one<KR, KC, 14>(P, fwd, st);
+        case 15: return launch_one<KR, KC, 15>(P, fwd, st);
+        case 16: return launch_one<KR, KC, 16>(P, fwd, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+#define MC_CAT2(a, b) a##b
+#define MC_CAT(a, b) MC_CAT2(a, b)
+
+cudaError_t MC_CAT(launch_cols_kr, MC_KR)(const FourParams &P, int KC, int NT, bool fwd,
+                                          cudaStream_t st) {
+#if MC_KR == 4
+    switch (KC) {  // K = 14, 15, 16
+        case 10: return launch_nt<4, 10>(P, NT, fwd, st);
+        case 11: return launch_nt<4, 11>(P, NT, fwd, st);
+        case 12: return launch_nt<4, 12>(P, NT, fwd, st);
+        default: return cudaErrorInvalidValue;
+    }
+#else
+    if (KC != 12) return cudaErrorInvalidValue;
+    return launch_nt<MC_KR, 12>(P, NT, fwd, st);
+#endif
+}
+
+}  // namespace mc

@@ -1,0 +1,87 @@
+// Internal definitions shared by the four-step compilation units
+// (fourstep.cu: row pass + orchestration; fourstep_cols.cu: column passes,
+// one unit per column size KR).
+#pragma once
+#include "conv_small.cuh"
+#include "fourstep.cuh"
+
+namespace mc {
+
+// Twiddle powers w_L^e for any e < L: lo[e & 4095] (plain) times hi[e >> 12]
+// (Shoup pair).  Forward (w) and inverse (w^-1) sets.
+struct TwistTabs {
+    const u32 *lo_f;
+    const uint2 *hi_f;
+    const u32 *lo_i;
+    const uint2 *hi_i;
+    double two32_over_p;  // 2^32 / p, for Shoup companions computed on the fly
+};
+
+struct FourParams {
+    ConvSmallParams cs;  // p, pinv, linv_mont (for the full L), level constants
+    const u32 *a;
+    const u32 *b;
+    u32 *c;
+    long long lda, ldb, ldc;
+    long long z1, z2, n;
+    u32 *Ah;  // scratch: [chunk][L] transformed a, later the product spectrum
+    u32 *Bh;  // scratch: [chunk][L] transformed b
+    long long prod0;  // first product of this chunk
+    int chunk;
+    int reduce;  // inputs are arbitrary words: reduce mod p on load
+    u32 red_wp;  // floor(2^32 / p)
+    TwistTabs tw;
+    const uint2 *col_tf, *col_ti;  // stage tables for the R-point column transforms
+    const uint2 *row_tf, *row_ti;  // stage tables for the C-point row transforms
+    long long nrows;  // rows of each product the row pass transforms (NT * R/16)
+};
+
+__device__ __forceinline__ u32 pow_w(const u32 *lo, const uint2 *hi, u32 e, u32 p) {
+    const uint2 h = __ldg(hi + (e >> 12));
+    return mul_shoup(__ldg(lo + (e & 4095)), h.x, h.y, p);
+}
+
+// floor(w * 2^32 / p) via a double estimate and one exact correction step.
+__device__ __forceinline__ u32 shoup_comp(u32 w, u32 p, double two32_over_p) {
+    u32 q = __double2uint_rz((double)w * two32_over_p);
+    long long r = (long long)(((unsigned long long)w << 32) - (unsigned long long)q * p);
+    if (r < 0) --q;
+    else if (r >= (long long)p) ++q;
+    return q;
+}
+
+
+template <int KR>
+struct ColCfg {
+    static constexpr int R = 1 << KR;
+    static constexpr int TC = 16384 >> KR;  // columns per tile (tile = 16K words)
+    static constexpr int THREADS = 1024;
+    static constexpr int G = R / 16;
+    // both column stage tables (the truncated inverse needs w and w^-1) + tile
+    static constexpr int SMEM = 2 * R * 8 + 16384 * 4;
+};
+
+// Column passes for one KR; NT = active top blocks of the column transform
+// (16 = full; < 16 = truncated: rows >= NT*R/16 are never formed).
+cudaError_t launch_cols_kr4(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
+cudaError_t launch_cols_kr5(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
+cudaError_t launch_cols_kr6(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
+cudaError_t launch_cols_kr7(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
+cudaError_t launch_cols_kr8(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
+cudaError_t launch_cols_kr9(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
+cudaError_t launch_cols_kr10(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
+cudaError_t launch_cols_kr11(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
+cudaError_t launch_cols_kr12(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
+
+template <class KF>
+static cudaError_t prep_kernel(KF kern, int smem, int threads, int *per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    if (per_sm) {
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kern, threads, smem);
+        if (*per_sm < 1) *per_sm = 1;
+    }
+    return e;
+}
+
+}  // namespace mc

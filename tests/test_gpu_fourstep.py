@@ -121,3 +121,18 @@ def test_crt3_kernel_edges(orc):
     t = [torch.from_numpy(r.view(np.int32)).cuda() for r in rs]
     got = to_u32_np(mc.crt3(*t))
     assert np.array_equal(got, orc.crt3(*rs))
+
+
+@pytest.mark.parametrize("z1,z2", [((1 << 19) + 1, 1 << 19), ((1 << 21) + 3, (1 << 20) + 5),
+                                    (3_000_001, 1_194_304)])
+def test_fourstep_truncated_large(orc, z1, z2):
+    """Truncated (tft) engine past a power of two at L = 2^20..2^23: rows
+    beyond NT*R/16 are never formed; bit-exact vs the oracle, and identical
+    to the padded engine."""
+    p = P3
+    a = gen_device(70, 0, z1, 1, z1, p)
+    b = gen_device(70, 1, z2, 1, z2, p)
+    c = mc.conv_batch(a, b, p, engine="tft")
+    want, _, _ = orc.conv_batch(to_u32_np(a), to_u32_np(b), p, orc.ENGINE_FFT_PAD)
+    assert np.array_equal(to_u32_np(c), want)
+    assert torch.equal(c, mc.conv_batch(a, b, p, engine="fft_pad"))
