@@ -423,6 +423,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
+    ap.add_argument("--engine", default=None, choices=["tft", "fft_pad"],
+                    help="override the config's engine (analysis only)")
     ap.add_argument("--ref-seconds", type=float, default=10.0,
                     help="target CPU seconds of the cpu_baseline sample")
     ap.add_argument("--ref-step-seconds", type=float, default=2.0,
@@ -430,7 +432,10 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.engine:  # analysis override (e.g. fft_pad on config 2's shapes)
+        cfg["engine"] = args.engine
+        cfg["name"] += f"_engine_{args.engine}"
     if args.impl == "reference":
         run_reference(args, cfg)
     else:

@@ -46,6 +46,7 @@ _SIGS = {
     "mc_conv_host_async": ([ctypes.c_int, vp, i64, i32, vp, i64, i32, vp, i64, i64, u32, i64,
                             vp], ctypes.c_int),
     "mc_gen_u32": ([u64, u64, u64, i64, i64, u64, vp, i64, vp], ctypes.c_int),
+    "mc_ubench_pass": ([ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
     "mc_ubench_int_pipes": ([ctypes.POINTER(ctypes.c_double), ctypes.c_int,
                              ctypes.POINTER(ctypes.c_double)], ctypes.c_int),
 }

@@ -40,9 +40,89 @@ __global__ void __launch_bounds__(256) ubench_kernel(u32 *out, u32 seed, int ite
     if (acc == 0x12345678u) out[0] = acc;  // keep the work live
 }
 
+// A radix-16 DIF register pass on two operands (32 butterflies each, one
+// LDS.64 twiddle per butterfly) repeated `iters` times with no exchange and
+// no barrier: the butterfly stream of conv_small_kernel in isolation.
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) pass_bench_kernel(const uint2 *tw_g, u32 *out,
+                                                                int iters, u32 p) {
+    __shared__ uint2 tw[4096];
+    for (int i = threadIdx.x; i < 4096; i += 256) tw[i] = tw_g[i];
+    __syncthreads();
+    const int t = threadIdx.x;
+    u32 va[16], vb[16];
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        va[s] = (t * 2654435761u + s * 40503u) % p;
+        vb[s] = (t * 2246822519u + s * 97u) % p;
+    }
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int lv = 3; lv >= 0; --lv) {
+            const int H = 1 << lv;
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                if (s & H) continue;
+                const uint2 w = tw[(H * 256 + t + 16 * (s & (2 * H - 1))) & 4095];
+                bfly_dif(va[s], va[s + H], w.x, w.y, p);
+                bfly_dif(vb[s], vb[s + H], w.x, w.y, p);
+            }
+        }
+    }
+    u32 acc = 0;
+#pragma unroll
+    for (int s = 0; s < 16; ++s) acc ^= va[s] ^ vb[s];
+    if (acc == 0x12345678u) out[0] = acc;
+}
+
 }  // namespace mc
 
 extern "C" {
+
+// Butterflies per clock per SM of the isolated register pass, at 2 and 4
+// resident 256-thread CTAs per SM (rates[0], rates[1]).
+mc_status mc_ubench_pass(double *rates) {
+    using namespace mc;
+    const int sms = sm_count();
+    int dev = current_device(), clk_khz = 0;
+    cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
+    const u32 p = 2013265921u;
+    uint2 *tw = nullptr;
+    u32 *out = nullptr;
+    MC_CUDA_CHECK(cudaMalloc(&tw, 4096 * sizeof(uint2)));
+    MC_CUDA_CHECK(cudaMalloc(&out, 4));
+    {
+        uint2 h[4096];
+        for (int i = 0; i < 4096; ++i) {
+            Shoup s = shoup((u32)((i * 7919ull + 1) % p), p);
+            h[i] = make_uint2(s.w, s.wp);
+        }
+        MC_CUDA_CHECK(cudaMemcpy(tw, h, sizeof(h), cudaMemcpyHostToDevice));
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    const int iters = 200;
+    for (int k = 0; k < 2; ++k) {
+        const int per_sm = k == 0 ? 2 : 4;
+        const int blocks = sms * per_sm;
+        for (int rep = 0; rep < 2; ++rep) {
+            cudaEventRecord(e0);
+            if (k == 0) pass_bench_kernel<2><<<blocks, 256>>>(tw, out, iters, p);
+            else pass_bench_kernel<4><<<blocks, 256>>>(tw, out, iters, p);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+        }
+        float ms = 0;
+        cudaEventElapsedTime(&ms, e0, e1);
+        const double bf = (double)blocks * 256 * iters * 64;
+        rates[k] = bf / (ms * 1e-3 * clk_khz * 1e3) / sms;
+    }
+    cudaFree(tw);
+    cudaFree(out);
+    MC_CUDA_CHECK(cudaGetLastError());
+    return MC_OK;
+}
 
 // rates[k] = thread-level operations per clock per SM for kind k
 // (0 IMAD, 1 IMAD.HI, 2 VIADDMNMX, 3 IADD3, 4 Shoup mul, 5 DIT butterfly),

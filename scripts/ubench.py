@@ -9,6 +9,10 @@ mhz = ctypes.c_double()
 _native.check(_native.lib().mc_ubench_int_pipes(rates, 6, ctypes.byref(mhz)))
 names = ["IMAD", "IMAD.HI", "VIADDMNMX", "IADD3", "shoup_mul_red", "dit_butterfly"]
 d = {n: rates[i] for i, n in enumerate(names)}
+pr = (ctypes.c_double * 2)()
+_native.check(_native.lib().mc_ubench_pass(pr))
+d["pass_bf_per_clk_sm_2cta"] = pr[0]
+d["pass_bf_per_clk_sm_4cta"] = pr[1]
 d["clock_mhz_attr"] = mhz.value
 d["sms"] = torch.cuda.get_device_properties(0).multi_processor_count
 print(json.dumps(d))
