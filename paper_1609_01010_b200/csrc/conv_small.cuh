@@ -500,13 +500,25 @@ conv_small_kernel(const ConvSmallParams P) {
         {
             constexpr int LAST = Plan<K>::NP - 1;
             constexpr int SB = (Plan<K>::NP == 0) ? (K - 4) : Plan<K>::sb(LAST < 0 ? 0 : LAST);
+            if constexpr (NT < 16 && SB + 4 <= K - 4) {
+                // all 16 slots of a thread sit in one G-block: one predicate
+                if ((slot_pos<SB>(t, 0) >> (K - 4)) < NT) {
 #pragma unroll
-            for (int s = 0; s < 16; ++s) {
-                const int x = slot_pos<SB>(t, s);
-                if (NT >= 16 || (x >> (K - 4)) < NT)
-                    va[s] = mul_shoup(mont_mul(va[s], vb[s], P.p, P.pinv), P.linv_mont, P.p);
-                else
-                    va[s] = 0u;  // time values of the inactive tail: u_j = 0
+                    for (int s = 0; s < 16; ++s)
+                        va[s] = mul_shoup(mont_mul(va[s], vb[s], P.p, P.pinv), P.linv_mont, P.p);
+                } else {
+#pragma unroll
+                    for (int s = 0; s < 16; ++s) va[s] = 0u;  // inactive tail: u_j = 0
+                }
+            } else {
+#pragma unroll
+                for (int s = 0; s < 16; ++s) {
+                    const int x = slot_pos<SB>(t, s);
+                    if (NT >= 16 || (x >> (K - 4)) < NT)
+                        va[s] = mul_shoup(mont_mul(va[s], vb[s], P.p, P.pinv), P.linv_mont, P.p);
+                    else
+                        va[s] = 0u;  // time values of the inactive tail: u_j = 0
+                }
             }
         }
 
