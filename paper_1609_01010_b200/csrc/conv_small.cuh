@@ -414,7 +414,8 @@ conv_small_kernel(const ConvSmallParams P) {
     uint2 *tf_s = reinterpret_cast<uint2 *>(smem_raw);
     uint2 *ti_s = tf_s + L;
     u32 *data = reinterpret_cast<u32 *>(ti_s + L);
-    {
+    const bool tma = C::PPC == 1 && P.tma;
+    if (!tma) {
         const uint4 *gf = reinterpret_cast<const uint4 *>(P.tf);
         const uint4 *gi = reinterpret_cast<const uint4 *>(P.ti);
         uint4 *sf = reinterpret_cast<uint4 *>(tf_s);
@@ -433,20 +434,24 @@ conv_small_kernel(const ConvSmallParams P) {
     uint64_t *mbar = reinterpret_cast<uint64_t *>(data + C::PPC * 2 * L);
     u32 *stA = reinterpret_cast<u32 *>(mbar + 2);
     u32 *stB = stA + P.za16;
-    const bool tma = C::PPC == 1 && P.tma;
-    auto prefetch = [&](long long r) {  // thread 0 only
+    auto prefetch = [&](long long r, u32 extra_bytes) {  // thread 0 only
         const u32 ba = 4u * P.za16, bb = 4u * P.zb16;
         fence_proxy_async_smem();
-        mbar_arrive_expect_tx(mbar, ba + bb);
+        mbar_arrive_expect_tx(mbar, ba + bb + extra_bytes);
         if (ba) bulk_g2s(stA, P.a + r * P.lda, ba, mbar);
         if (bb) bulk_g2s(stB, P.b + r * P.ldb, bb, mbar);
     };
     if (tma && threadIdx.x == 0) {
+        // one DRAM round trip for the prologue: the stage tables and the
+        // first product's rows all land on the first mbarrier phase (the
+        // grid never exceeds the batch, so every CTA owns a product)
         mbar_init(mbar, 1);
         fence_mbar_init();
+        prefetch(blockIdx.x, 2u * L * 8u);
+        bulk_g2s(tf_s, P.tf, L * 8u, mbar);
+        bulk_g2s(ti_s, P.ti, L * 8u, mbar);
     }
     __syncthreads();
-    if (tma && threadIdx.x == 0 && (long long)blockIdx.x < P.batch) prefetch(blockIdx.x);
     uint32_t phase = 0;
 
     for (long long base = (long long)blockIdx.x * C::PPC; base < P.batch;
@@ -475,7 +480,7 @@ conv_small_kernel(const ConvSmallParams P) {
             }
             __syncthreads();  // staging consumed: refill it for the next product
             const long long nxt = base + (long long)gridDim.x * C::PPC;
-            if (threadIdx.x == 0 && nxt < P.batch) prefetch(nxt);
+            if (threadIdx.x == 0 && nxt < P.batch) prefetch(nxt, 0u);
         } else {
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
