@@ -20,7 +20,8 @@ struct RowCfg {
 };
 
 template <int KC>
-__global__ void __launch_bounds__(RowCfg<KC>::THREADS, 2) row_conv_kernel(const FourParams P,
+__global__ void __launch_bounds__(RowCfg<KC>::THREADS, RowCfg<KC>::THREADS >= 512 ? 1 : 2)
+row_conv_kernel(const FourParams P,
                                                                           int KR) {
     using RC = RowCfg<KC>;
     constexpr int Cn = RC::C, T = RC::T, G = Cn / 16;
@@ -203,6 +204,7 @@ static cudaError_t launch_rows_any(int KC, int KR, const FourParams &P, cudaStre
         case 10: return launch_rows<10>(P, KR, st);
         case 11: return launch_rows<11>(P, KR, st);
         case 12: return launch_rows<12>(P, KR, st);
+        case 13: return launch_rows<13>(P, KR, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -222,7 +224,18 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     const FieldTables *TL, *TR, *TC;
     mc_status s = get_tables(p, K, &TL);
     if (s != MC_OK) return s;
-    const int KC = std::min(12, K - 4), KR = K - KC;
+    // Row length C = 2^KC: 2^12 (measured better than 2^13 at K = 23, whose
+    // wider column tiles do not pay for the 1-CTA/SM K=13 row pass);
+    // MC_FOURSTEP_KC overrides for A/B runs.
+    static const int kc_env = [] {
+        const char *e = getenv("MC_FOURSTEP_KC");
+        return e ? atoi(e) : 0;
+    }();
+    int KC = std::min(12, K - 4);
+    if (kc_env >= 10 && kc_env <= 13 && K - kc_env >= 4 && K - kc_env <= 12 &&
+        (kc_env == 12 || kc_env == 13 || K - kc_env == 4))
+        KC = kc_env;
+    const int KR = K - KC;
     if ((s = get_tables(p, KR, &TR)) != MC_OK) return s;
     if ((s = get_tables(p, KC, &TC)) != MC_OK) return s;
     FourParams P;

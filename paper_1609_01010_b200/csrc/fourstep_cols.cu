@@ -12,7 +12,7 @@ namespace mc {
 // 16): top-pass outputs of blocks >= NT are pruned, lower passes skip those
 // blocks and only rows < NT*R/16 are written.
 template <int KR, int KC, int NT>
-__global__ void __launch_bounds__(1024, 1) col_fwd_kernel(const FourParams P) {
+__global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_fwd_kernel(const FourParams P) {
     using C = ColCfg<KR>;
     constexpr long long Ccols = 1ll << KC;
     extern __shared__ uint4 smem_raw[];
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(1024, 1) col_fwd_kernel(const FourParams P) {
 // >= NT*R/16 hold the column time values, which are zero for a product of
 // length <= NT*L/16, then the van der Hoeven top pass (ItftTop).
 template <int KR, int KC, int NT>
-__global__ void __launch_bounds__(1024, 1) col_inv_kernel(const FourParams P) {
+__global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_inv_kernel(const FourParams P) {
     using C = ColCfg<KR>;
     constexpr long long Ccols = 1ll << KC;
     extern __shared__ uint4 smem_raw[];
@@ -143,6 +143,12 @@ cudaError_t MC_CAT(launch_cols_kr, MC_KR)(const FourParams &P, int KC, int NT, b
         case 10: return launch_nt<4, 10>(P, NT, fwd, st);
         case 11: return launch_nt<4, 11>(P, NT, fwd, st);
         case 12: return launch_nt<4, 12>(P, NT, fwd, st);
+        default: return cudaErrorInvalidValue;
+    }
+#elif MC_KR >= 9 && MC_KR <= 11
+    switch (KC) {  // K = 21..24 may use 2^13 rows
+        case 12: return launch_nt<MC_KR, 12>(P, NT, fwd, st);
+        case 13: return launch_nt<MC_KR, 13>(P, NT, fwd, st);
         default: return cudaErrorInvalidValue;
     }
 #else

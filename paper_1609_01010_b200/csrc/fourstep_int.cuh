@@ -51,14 +51,24 @@ __device__ __forceinline__ u32 shoup_comp(u32 w, u32 p, double two32_over_p) {
 }
 
 
+#ifndef MC_COL_TILE
+#define MC_COL_TILE 16384
+#endif
+
+// Column tile: R rows x TC columns = MC_COL_TILE words, one 16-slot column
+// transform per R/16 threads.  16K-word tiles (1024 threads, 1 CTA/SM)
+// measured faster than 8K tiles with 2 CTAs/SM (narrower row segments cost
+// more than the load/compute overlap gained).
 template <int KR>
 struct ColCfg {
     static constexpr int R = 1 << KR;
-    static constexpr int TC = 16384 >> KR;  // columns per tile (tile = 16K words)
-    static constexpr int THREADS = 1024;
+    static constexpr int TILE = MC_COL_TILE;
+    static constexpr int TC = TILE >> KR;  // columns per tile
+    static constexpr int THREADS = TILE / 16;
     static constexpr int G = R / 16;
+    static constexpr int MINB = THREADS >= 1024 ? 1 : 2;
     // both column stage tables (the truncated inverse needs w and w^-1) + tile
-    static constexpr int SMEM = 2 * R * 8 + 16384 * 4;
+    static constexpr int SMEM = 2 * R * 8 + TILE * 4;
 };
 
 // Column passes for one KR; NT = active top blocks of the column transform
