@@ -375,6 +375,14 @@ def run_mine(args, cfg):
         alg_bytes = 4 * (z1 + z2 + n) * B
         bytes_note = "compulsory 4*(z1+z2+n) per product (fused single pass)"
     kern_ms = statistics.mean(times)  # one launch of the fused kernel per step (cfg 1-3)
+    traffic = None
+    try:  # DRAM bytes per launch from the committed ncu capture of this workload
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(cfg["name"])
+        if tr:
+            traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+    except Exception:
+        traffic = None
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
     from paper_1609_01010_b200.transform import full_count, itft_count, tft_count
 
@@ -399,7 +407,7 @@ def run_mine(args, cfg):
                    "launch": "cuda graph replay" if graph is not None else "eager"},
         "gcoeff_per_s": value * n / 1e9,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "alg_bytes_per_step": alg_bytes, "bytes_model": bytes_note,
                      "kernel_ms": kern_ms},
         "int_pipe": {"butterflies_per_product": bf, "pointwise_per_product": pw,
