@@ -89,6 +89,28 @@ mc_status mc_conv_tft(const uint32_t *a, int64_t lda, int32_t z1,
 mc_status mc_circ_conv(const uint32_t *u, const uint32_t *v, uint32_t *w,
                        int32_t log2L, int64_t batch, uint32_t p, void *stream);
 
+/* Eq. 13 split engine.  Residues of each row u (length
+ * 2n) mod x^n - 1 and mod x^n + 1: a_j = u_j + u_{j+n}, b_j = u_j - u_{j+n}
+ * (convolve.py:214-219 split_residues); u: [batch][2n], a, b: [batch][n]. */
+mc_status mc_split_residues(const uint32_t *u, uint32_t *a, uint32_t *b, int32_t log2n,
+                            int64_t batch, uint32_t p, void *stream);
+
+/* Inverse of mc_split_residues: w_j = (a_j + b_j)/2, w_{j+n} = (a_j - b_j)/2
+ * (convolve.py:222-227 recombine_residues). */
+mc_status mc_recombine_residues(const uint32_t *a, const uint32_t *b, uint32_t *w,
+                                int32_t log2n, int64_t batch, uint32_t p, void *stream);
+
+/* Batched negacyclic convolution of length n (product mod x^n + 1) by
+ * twisting with psi = w_2n (convolve.py:172-190 nega_conv); needs
+ * log2(2n) <= two_adicity(p). */
+mc_status mc_nega_conv(const uint32_t *u, const uint32_t *v, uint32_t *w, int32_t log2n,
+                       int64_t batch, uint32_t p, void *stream);
+
+/* Batched circular convolution of length L = 2n through the split into a
+ * circular and a negacyclic half (convolve.py:193-211 circ_conv_split). */
+mc_status mc_circ_conv_split(const uint32_t *u, const uint32_t *v, uint32_t *w, int32_t log2L,
+                             int64_t batch, uint32_t p, void *stream);
+
 /* Batched full transform, natural order in and out; inverse applies the
  * 1/L scale (transform.py:167-196 moddft).  x, y: [batch][L]. */
 mc_status mc_ntt(const uint32_t *x, uint32_t *y, int32_t log2L, int64_t batch,

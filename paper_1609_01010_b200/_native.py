@@ -35,6 +35,10 @@ _SIGS = {
     "mc_conv_tft": ([vp, i64, i32, vp, i64, i32, vp, i64, i64, u32, vp], ctypes.c_int),
     "mc_circ_conv": ([vp, vp, vp, i32, i64, u32, vp], ctypes.c_int),
     "mc_ntt": ([vp, vp, i32, i64, u32, ctypes.c_int, vp], ctypes.c_int),
+    "mc_split_residues": ([vp, vp, vp, i32, i64, u32, vp], ctypes.c_int),
+    "mc_recombine_residues": ([vp, vp, vp, i32, i64, u32, vp], ctypes.c_int),
+    "mc_nega_conv": ([vp, vp, vp, i32, i64, u32, vp], ctypes.c_int),
+    "mc_circ_conv_split": ([vp, vp, vp, i32, i64, u32, vp], ctypes.c_int),
     "mc_tft": ([vp, i32, vp, i32, i32, i64, u32, vp], ctypes.c_int),
     "mc_itft": ([vp, vp, i32, i32, i64, u32, vp], ctypes.c_int),
     "mc_crt3": ([vp, vp, vp, vp, i64, vp], ctypes.c_int),

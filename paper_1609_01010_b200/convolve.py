@@ -7,12 +7,15 @@ and poly_mul (:264-296), plus a batched tensor API (conv_batch) that is the
 hot path proper: [B, z1] x [B, z2] -> [B, n] in one kernel launch.
 
 Engines run in libmodconv_b200 (mc_conv_fft_pad / mc_conv_tft /
-mc_circ_conv).  `threads` is accepted and ignored (the GPU does not use host
-workers; results are schedule-independent like the reference's).  The
-quadratic "definition" engine is a CPU oracle in the reference; here it is
-served by the GPU fft_pad kernel (bit-identical output, no counters touched,
-exactly as lin_conv_def touches none).  "split" (Eq. 13) is not on the
-north-star path and raises.
+mc_circ_conv / mc_circ_conv_split).  `threads` is accepted and ignored (the
+GPU does not use host workers; results are schedule-independent like the
+reference's).  The quadratic "definition" engine is a CPU oracle in the
+reference; here it is served by the GPU fft_pad kernel (bit-identical
+output, no counters touched, exactly as lin_conv_def touches none).  The
+Eq. 13 "split" engine (nega_conv, circ_conv_split, split_residues,
+recombine_residues: convolve.py:172-227) runs on the GPU as two half-length
+circular convolutions around fused split/twist and untwist/recombine
+kernels.
 """
 
 from __future__ import annotations
@@ -199,6 +202,91 @@ def conv_tft(g, h, req: ConvRequest) -> list[int]:
     return out
 
 
+# ------------------------------------------------------------------ split engine
+def _pow2_len(n: int, what: str = "length") -> int:
+    if n == 0 or n & (n - 1):
+        raise ValueError(f"{what} must be a power of two: {n}")
+    return n.bit_length() - 1
+
+
+def split_residues(u, p: int) -> tuple[list[int], list[int]]:
+    """Residues of u mod (x^n - 1) and mod (x^n + 1), n = len(u)/2
+    (convolve.py:214-219), on the GPU."""
+    size = len(u)
+    lg = _pow2_len(size) - 1 if size >= 2 else None
+    if lg is None:
+        raise ValueError("length must be a power of two >= 2")
+    dev = _tensors.require_cuda()
+    x = _tensors.list_to_device(u, p, dev)
+    a = torch.empty(size // 2, dtype=torch.int32, device=dev)
+    b = torch.empty_like(a)
+    _native.check(_native.lib().mc_split_residues(_tensors.ptr(x), _tensors.ptr(a),
+                                                  _tensors.ptr(b), lg, 1, p,
+                                                  _tensors.stream_handle()))
+    return _tensors.device_to_list(a), _tensors.device_to_list(b)
+
+
+def recombine_residues(a, b, p: int) -> list[int]:
+    """Inverse of split_residues (convolve.py:222-227), on the GPU."""
+    if len(a) != len(b):
+        raise ValueError("residue halves must have equal lengths")
+    lg = _pow2_len(len(a))
+    dev = _tensors.require_cuda()
+    x = _tensors.list_to_device(a, p, dev)
+    y = _tensors.list_to_device(b, p, dev)
+    w = torch.empty(2 * len(a), dtype=torch.int32, device=dev)
+    _native.check(_native.lib().mc_recombine_residues(_tensors.ptr(x), _tensors.ptr(y),
+                                                      _tensors.ptr(w), lg, 1, p,
+                                                      _tensors.stream_handle()))
+    return _tensors.device_to_list(w)
+
+
+def nega_conv(u, v, req: ConvRequest) -> list[int]:
+    """Negacyclic convolution (product mod x^n + 1) via the psi twist
+    (convolve.py:172-190).  Needs 2-adicity >= log2(2n)."""
+    n = len(u)
+    if n == 0 or len(v) != n:
+        raise ValueError(f"need equal nonempty lengths, got {len(u)} and {len(v)}")
+    lg = _pow2_len(n)
+    fp = as_field(req.field)
+    check_transform_size(fp, lg + 1)
+    dev = _tensors.require_cuda()
+    a = _tensors.list_to_device(u, fp.p, dev)
+    b = _tensors.list_to_device(v, fp.p, dev)
+    c = torch.empty_like(a)
+    _native.check(_native.lib().mc_nega_conv(_tensors.ptr(a), _tensors.ptr(b), _tensors.ptr(c),
+                                             lg, 1, fp.p, _tensors.stream_handle()))
+    if req.counters is not None:
+        req.counters.butterflies += 3 * full_count(n)
+        req.counters.pointwise_muls += n
+    return _tensors.device_to_list(c)
+
+
+def circ_conv_split(u, v, req: ConvRequest) -> list[int]:
+    """Circular convolution of length 2n via the (x^n - 1)/(x^n + 1) split
+    (convolve.py:193-211)."""
+    size = len(u)
+    if size == 0 or len(v) != size:
+        raise ValueError(f"need equal nonempty lengths, got {len(u)} and {len(v)}")
+    if size & (size - 1) or size < 2:
+        raise ValueError(f"length must be a power of two >= 2: {size}")
+    fp = as_field(req.field)
+    lg = size.bit_length() - 1
+    check_transform_size(fp, lg)
+    dev = _tensors.require_cuda()
+    a = _tensors.list_to_device(u, fp.p, dev)
+    b = _tensors.list_to_device(v, fp.p, dev)
+    c = torch.empty_like(a)
+    _native.check(_native.lib().mc_circ_conv_split(_tensors.ptr(a), _tensors.ptr(b),
+                                                   _tensors.ptr(c), lg, 1, fp.p,
+                                                   _tensors.stream_handle()))
+    if req.counters is not None:  # circ_conv_fft + nega_conv, both on n points
+        n = size // 2
+        req.counters.butterflies += 2 * 3 * full_count(n)
+        req.counters.pointwise_muls += 2 * n
+    return _tensors.device_to_list(c)
+
+
 def _resolve_engine(a_len: int, b_len: int, req: ConvRequest) -> str:
     if req.engine != "auto":
         return req.engine
@@ -232,7 +320,11 @@ def poly_mul(a, b, req: ConvRequest) -> DensePoly:
     elif engine == "tft":
         out = conv_tft(u, v, req)
     elif engine == "split":
-        raise ValueError("engine 'split' (convolve.py:193-227) is not provided by the GPU path")
+        out_len = len(u) + len(v) - 1
+        size = max(2, _next_pow2(out_len))
+        up = u + [0] * (size - len(u))
+        vp = v + [0] * (size - len(v))
+        out = circ_conv_split(up, vp, req)[:out_len]
     else:
         raise ValueError(f"unknown engine {engine!r}")
     return DensePoly(fp, tuple(out)).normalize()

@@ -156,6 +156,13 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
                          reduce);
 }
 
+// Batched circular convolution of length 2^log2L (split engine building block).
+mc_status circ_conv_dispatch(const u32 *u, const u32 *v, u32 *w, int log2L, long long batch,
+                             u32 p, cudaStream_t st) {
+    const long long L = 1ll << log2L;
+    return conv_dispatch(0, u, L, (int)L, v, L, (int)L, w, L, batch, p, st, log2L);
+}
+
 // Product mod p of two arbitrary-word vectors (three-primes channels).
 mc_status conv_dispatch_reduced(const u32 *a, int z1, const u32 *b, int z2, u32 *r, u32 p,
                                 cudaStream_t st) {

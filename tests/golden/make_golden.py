@@ -43,7 +43,14 @@ from modconv import (  # noqa: E402
     poly_mul,
     tft,
 )
-from modconv.convolve import conv_tft, lin_conv_fft_pad  # noqa: E402
+from modconv.convolve import (  # noqa: E402
+    circ_conv_split,
+    conv_tft,
+    lin_conv_fft_pad,
+    nega_conv,
+    recombine_residues,
+    split_residues,
+)
 
 from oracle import oracle  # noqa: E402  (only for the shared input generator)
 
@@ -175,6 +182,40 @@ def poly_cases(rng):
     return out
 
 
+def split_cases(rng):
+    """Eq. 13 split engine (convolve.py:172-227) at several sizes and primes."""
+    out = []
+    for p in (17, 257, P2, P3):
+        fp = FourierPrime.from_modulus(p)
+        for size in (2, 4, 8, 16, 64, 256, 1024):
+            if size.bit_length() - 1 > fp.two_adicity:
+                continue
+            u = [rng.randrange(p) for _ in range(size)]
+            v = [rng.randrange(p) for _ in range(size)]
+            cnt = OpCounters()
+            split = circ_conv_split(u, v, ConvRequest(fp, engine="split", counters=cnt))
+            a, b = split_residues(u, p)
+            entry = {"p": p, "size": size, "u": u, "v": v, "split": split,
+                     "split_counters": [cnt.butterflies, cnt.pointwise_muls],
+                     "res_a": a, "res_b": b, "recombined": recombine_residues(a, b, p)}
+            if size.bit_length() <= fp.two_adicity:  # nega_conv on `size` points needs 2*size
+                cn = OpCounters()
+                entry["nega"] = nega_conv(u, v, ConvRequest(fp, counters=cn))
+                entry["nega_counters"] = [cn.butterflies, cn.pointwise_muls]
+            out.append(entry)
+    for p in (P2, P3):  # poly_mul with the split engine (normalize + counters)
+        fp = FourierPrime.from_modulus(p)
+        for z1, z2 in ((1, 1), (3, 7), (100, 28), (129, 1)):
+            u = [rng.randrange(1, p) for _ in range(z1)]
+            v = [rng.randrange(1, p) for _ in range(z2)]
+            cnt = OpCounters()
+            r = poly_mul(DensePoly(fp, tuple(u)), DensePoly(fp, tuple(v)),
+                         ConvRequest(fp, engine="split", counters=cnt))
+            out.append({"p": p, "poly": True, "u": u, "v": v, "out": list(r.coeffs),
+                        "counters": [cnt.butterflies, cnt.pointwise_muls]})
+    return out
+
+
 def config_row(cfg, p, z1, z2, seed, rows, engine):
     """Reference poly_mul on rows of a BASELINE config (shared seeded inputs)."""
     fp = FourierPrime.from_modulus(p)
@@ -247,6 +288,7 @@ def main():
         "transforms": transforms(rng),
         "convs": convs(rng),
         "poly_mul": poly_cases(rng),
+        "split": split_cases(random.Random(0x5117)),
     }
     with open(os.path.join(HERE, "reference_small.json"), "w") as f:
         json.dump(small, f, separators=(",", ":"))
