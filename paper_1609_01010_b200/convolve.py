@@ -91,8 +91,8 @@ def conv_batch(a: torch.Tensor, b: torch.Tensor, field, engine: str = "tft",
     engine: "tft" (truncated transforms, convolve.py:230-253) or "fft_pad"
     (zero-padded full transforms, convolve.py:160-169).
     """
-    if engine not in ("tft", "fft_pad"):
-        raise ValueError(f"batched engine must be 'tft' or 'fft_pad', got {engine!r}")
+    if engine not in ("tft", "fft_pad", "auto"):
+        raise ValueError(f"batched engine must be 'tft', 'fft_pad' or 'auto', got {engine!r}")
     fp = as_field(field)
     a = _as_batch(a, "a")
     b = _as_batch(b, "b")
@@ -105,6 +105,8 @@ def conv_batch(a: torch.Tensor, b: torch.Tensor, field, engine: str = "tft",
     n = z1 + z2 - 1
     check_transform_size(fp, (_next_pow2(n)).bit_length() - 1)
     dev = _tensors.require_cuda()
+    if engine == "auto":  # GPU-timed choice per size class (planner.GpuPlanner)
+        engine = default_planner().resolve_engine(fp, z1, z2)
     host = a.device.type == "cpu"
     if host != (b.device.type == "cpu"):
         raise ValueError("a and b must be on the same device")
@@ -148,6 +150,19 @@ def _conv_batch_host(a, b, fp, engine, out, counters, stream) -> torch.Tensor:
     st.synchronize()
     count_engine(engine, z1, z2, counters, B)
     return out if out is not None else c_h
+
+
+_DEFAULT_PLANNER = None
+
+
+def default_planner():
+    """Process-wide GpuPlanner used by conv_batch(engine="auto")."""
+    global _DEFAULT_PLANNER
+    if _DEFAULT_PLANNER is None:
+        from .planner import GpuPlanner
+
+        _DEFAULT_PLANNER = GpuPlanner()
+    return _DEFAULT_PLANNER
 
 
 # ------------------------------------------------------------------ list API
