@@ -14,6 +14,15 @@ from dataclasses import dataclass
 from .field import FieldMismatchError, FourierPrime, as_field
 
 
+class PolyTextError(ValueError):
+    """Malformed polynomial text; `line` is the 1-based offending line
+    (poly.py:14-19 of the reference)."""
+
+    def __init__(self, message: str, line: int):
+        super().__init__(f"line {line}: {message}")
+        self.line = line
+
+
 @dataclass(frozen=True, slots=True)
 class DensePoly:
     field: FourierPrime
@@ -70,3 +79,44 @@ class DensePoly:
 def check_same_field(a, b) -> None:
     if a.field.p != b.field.p:
         raise FieldMismatchError(f"mixed moduli {a.field.p} and {b.field.p}")
+
+
+# ------------------------------------------------------------------ text format
+# Interchange format of the reference CLI (poly.py:184-223): three lines --
+# the modulus, the coefficient count, the space-separated residues.
+
+def poly_to_text(a) -> str:
+    return f"{a.field.p}\n{len(a.coeffs)}\n{' '.join(str(int(c)) for c in a.coeffs)}\n"
+
+
+def _parse_int(token: str, what: str, line: int) -> int:
+    try:
+        return int(token)
+    except ValueError:
+        raise PolyTextError(f"bad {what} {token!r}", line) from None
+
+
+def poly_from_text(text: str, field=None) -> DensePoly:
+    """Parse the three-line format; errors carry the offending line."""
+    head = text.splitlines()
+    if len(head) < 3:
+        raise PolyTextError("expected 3 lines: modulus, count, coefficients", len(head) + 1)
+    modulus_line, count_line, coeff_line = head[0], head[1], head[2]
+    p = _parse_int(modulus_line, "modulus", 1)
+    if field is not None and field.p == p:
+        fp = as_field(field)
+    else:
+        try:
+            fp = as_field(p)
+        except ValueError as exc:
+            raise PolyTextError(str(exc), 1) from None
+    count = _parse_int(count_line, "coefficient count", 2)
+    if count < 0:
+        raise PolyTextError(f"negative coefficient count {count}", 2)
+    values = [_parse_int(tok, "coefficient", 3) for tok in coeff_line.split()]
+    if len(values) != count:
+        raise PolyTextError(f"expected {count} coefficients, found {len(values)}", 3)
+    bad = next((v for v in values if not 0 <= v < p), None)
+    if bad is not None:
+        raise PolyTextError(f"coefficient {bad} not a canonical residue mod {p}", 3)
+    return DensePoly(fp, tuple(values))
