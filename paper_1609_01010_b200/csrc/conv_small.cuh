@@ -310,6 +310,17 @@ struct Plan {
     static constexpr int sb(int i) { return lo(i); }
 };
 
+// A lower pass can skip inactive G-blocks only if every lane of a warp and
+// every slot of a thread lie in the same G-block (bits >= K-4 of the
+// position): then the skip is warp-uniform and removes whole warps' work.
+// Lane bit 4 lands on position bit 4 (SB >= 5) or 8 (SB <= 4); the slot
+// window is [SB, SB+4).  True for K >= 13 with SB in {0, 4}; never at K = 12,
+// where a warp straddles two G-blocks (there the branch only fences ptxas).
+template <int K, int SB>
+constexpr bool warp_uniform_blocks() {
+    return (SB + 3 < K - 4) && ((SB >= 5 ? 4 : 8) < K - 4);
+}
+
 template <int K, int I>
 __device__ __forceinline__ int gblock_of_pass(int t) {
     return slot_pos<Plan<K>::sb(I)>(t, 0) >> (K - 4);
@@ -327,12 +338,14 @@ __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[
         __syncthreads();
         get<SB>(bufA, va, t);
         get<SB>(bufB, vb, t);
-        // Inactive G-blocks (>= NT) are transformed too and discarded at the
-        // pointwise step: a warp spans two G-blocks, so a per-thread skip
-        // saves nothing for odd NT while its branch fences ptxas from
-        // overlapping the exchange with the butterflies (measured -9%).
-        fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(va, t, P, W);
-        fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(vb, t, P, W);
+        // Inactive G-blocks (>= NT) are skipped only where that is
+        // warp-uniform; elsewhere they are transformed and discarded at the
+        // pointwise step (a half-warp skip saves nothing and its branch
+        // fences ptxas from overlapping the exchange: measured -9% at K=12).
+        if (NT >= 16 || !warp_uniform_blocks<K, SB>() || gblock_of_pass<K, I>(t) < NT) {
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(va, t, P, W);
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(vb, t, P, W);
+        }
         fwd_lower_chain<K, NT, I + 1>(bufA, bufB, va, vb, t, P, W);
     }
 }
@@ -345,7 +358,8 @@ __device__ __forceinline__ void inv_lower_chain(u32 *buf, u32 (&v)[16], int t,
     if constexpr (I >= 0) {
         constexpr int SB = Plan<K>::sb(I);
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
-        inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(v, t, P, W);  // zeros stay zeros
+        if (NT >= 16 || !warp_uniform_blocks<K, SB>() || gblock_of_pass<K, I>(t) < NT)
+            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(v, t, P, W);  // zeros stay zeros
         __syncthreads();
         put<SB>(buf, v, t);
         __syncthreads();
