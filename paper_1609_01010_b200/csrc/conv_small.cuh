@@ -310,20 +310,33 @@ struct Plan {
     static constexpr int sb(int i) { return lo(i); }
 };
 
-// A lower pass can skip inactive G-blocks only if every lane of a warp and
-// every slot of a thread lie in the same G-block (bits >= K-4 of the
-// position): then the skip is warp-uniform and removes whole warps' work.
-// Lane bit 4 lands on position bit 4 (SB >= 5) or 8 (SB <= 4); the slot
-// window is [SB, SB+4).  True for K >= 13 with SB in {0, 4}; never at K = 12,
-// where a warp straddles two G-blocks (there the branch only fences ptxas).
+// Warp-level skipping of inactive G-blocks (truncated transforms).  A warp
+// may skip a lower pass when the lowest G-block it touches -- lane 0, slot 0
+// -- is inactive: every other slot/lane of the warp is then in a block at
+// least as high.  can_skip<K, I, NT>() is false when even the last warp
+// starts below NT (e.g. K = 12 with NT = 15, where a warp straddles two
+// G-blocks): the branch is then compiled out, since it only fences ptxas
+// from overlapping the exchange with the butterflies (measured -9%).
 template <int K, int SB>
-constexpr bool warp_uniform_blocks() {
-    return (SB + 3 < K - 4) && ((SB >= 5 ? 4 : 8) < K - 4);
+constexpr int gblock_const(int t) {
+    return (((t >> SB) << (SB + 4)) | (t & ((1 << SB) - 1))) >> (K - 4);
+}
+
+template <int K, int I, int NT>
+constexpr bool can_skip() {
+    constexpr int T = (1 << K) / 16;
+    return NT < 16 && T >= 32 && gblock_const<K, Plan<K>::sb(I)>(T - 32) >= NT;
 }
 
 template <int K, int I>
 __device__ __forceinline__ int gblock_of_pass(int t) {
     return slot_pos<Plan<K>::sb(I)>(t, 0) >> (K - 4);
+}
+
+template <int K, int I, int NT>
+__device__ __forceinline__ bool pass_active(int t) {
+    if constexpr (!can_skip<K, I, NT>()) return true;
+    else return gblock_of_pass<K, I>(t & ~31) < NT;  // warp-uniform
 }
 
 template <int K, int NT, int I>
@@ -338,11 +351,9 @@ __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[
         __syncthreads();
         get<SB>(bufA, va, t);
         get<SB>(bufB, vb, t);
-        // Inactive G-blocks (>= NT) are skipped only where that is
-        // warp-uniform; elsewhere they are transformed and discarded at the
-        // pointwise step (a half-warp skip saves nothing and its branch
-        // fences ptxas from overlapping the exchange: measured -9% at K=12).
-        if (NT >= 16 || !warp_uniform_blocks<K, SB>() || gblock_of_pass<K, I>(t) < NT) {
+        // Inactive G-blocks (>= NT) are skipped per warp where possible;
+        // otherwise transformed and discarded at the pointwise step.
+        if (pass_active<K, I, NT>(t)) {
             fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(va, t, P, W);
             fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(vb, t, P, W);
         }
@@ -358,7 +369,7 @@ __device__ __forceinline__ void inv_lower_chain(u32 *buf, u32 (&v)[16], int t,
     if constexpr (I >= 0) {
         constexpr int SB = Plan<K>::sb(I);
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
-        if (NT >= 16 || !warp_uniform_blocks<K, SB>() || gblock_of_pass<K, I>(t) < NT)
+        if (pass_active<K, I, NT>(t))
             inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB>(v, t, P, W);  // zeros stay zeros
         __syncthreads();
         put<SB>(buf, v, t);
