@@ -57,6 +57,31 @@ def _dist():
     return ws, rank, local
 
 
+def _int_roofline(bf: int, pw: int, products_per_s_per_gpu: float, peaks: dict) -> dict:
+    """Integer-pipe roofline: reference butterflies/s per GPU against the
+    practical ceiling measured on B200 by scripts/ubench.py (the fused
+    kernel's radix-16 register pass in isolation, committed in
+    profiles/r01/ubench.json) and against the nominal IMAD-pipe ceiling
+    (64 IMAD/clk/SM, 4 IMAD slots per Shoup butterfly)."""
+    achieved = bf * products_per_s_per_gpu
+    out = {"bound": "int_pipe", "unit": "butterflies/s", "achieved": achieved,
+           "butterflies_per_product": bf, "pointwise_per_product": pw,
+           "count": "reference OpCounters butterflies (algorithmic)"}
+    try:
+        with open(os.path.join(REPO, "profiles", "r01", "ubench.json")) as f:
+            ub = json.load(f)
+        mhz = float(peaks.get("sm_max_mhz", ub.get("clock_mhz_attr", 1965.0)))
+        sms = int(ub.get("sms", 148))
+        practical = ub["pass_bf_per_clk_sm_2cta"] * sms * mhz * 1e6
+        nominal = 16.0 * sms * mhz * 1e6
+        out.update({"peak": practical, "frac": achieved / practical,
+                    "peak_kind": "measured: isolated radix-16 pass, profiles/r01/ubench.json",
+                    "nominal_peak": nominal, "nominal_frac": achieved / nominal})
+    except Exception:
+        pass
+    return out
+
+
 def _coll_device(dev):
     """Device for collective tensors: the GPU under NCCL, the host under gloo."""
     import torch.distributed as dist
@@ -410,9 +435,7 @@ def run_mine(args, cfg):
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "alg_bytes_per_step": alg_bytes, "bytes_model": bytes_note,
                      "kernel_ms": kern_ms},
-        "int_pipe": {"butterflies_per_product": bf, "pointwise_per_product": pw,
-                     "gbutterflies_per_s": bf * value / ws / 1e9,
-                     "note": "integer-pipe bound; see DESIGN.md for the IMAD roofline"},
+        "int_pipe": _int_roofline(bf, pw, value / ws, peaks),
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk,

@@ -7,5 +7,5 @@ for f in sys.argv[1:]:
     r = d.get("roofline", {})
     print(f.split('/')[-1], f"{d['value']:.4g}", d['unit'], "kernel_ms", round(r.get('kernel_ms', 0), 4),
           "frac", round(r.get('frac', 0), 4), "e2e", f"{(d.get('e2e') or {}).get('value', 0):.4g}",
-          "Gbf/s", round(d.get('int_pipe', {}).get('gbutterflies_per_s', 0)), "clk", d.get('clocks', {}).get('sm_mhz'),
+          "int_frac", round(d.get('int_pipe', {}).get('frac', 0), 3), "clk", d.get('clocks', {}).get('sm_mhz'),
           d.get('clocks', {}).get('reasons'))
