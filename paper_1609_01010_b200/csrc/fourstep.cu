@@ -5,6 +5,8 @@
 #include <tuple>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "fourstep_int.cuh"
 
 namespace mc {
@@ -184,19 +186,60 @@ static cudaError_t launch_rows(const FourParams &P, int KR, cudaStream_t st) {
 }
 
 static cudaError_t launch_cols_any(int KC, int KR, int NT, const FourParams &P, bool fwd,
-                                   cudaStream_t st) {
+                                   cudaStream_t st, const ColTma *tma = nullptr) {
     switch (KR) {
-        case 4: return launch_cols_kr4(P, KC, NT, fwd, st);
-        case 5: return launch_cols_kr5(P, KC, NT, fwd, st);
-        case 6: return launch_cols_kr6(P, KC, NT, fwd, st);
-        case 7: return launch_cols_kr7(P, KC, NT, fwd, st);
-        case 8: return launch_cols_kr8(P, KC, NT, fwd, st);
-        case 9: return launch_cols_kr9(P, KC, NT, fwd, st);
-        case 10: return launch_cols_kr10(P, KC, NT, fwd, st);
-        case 11: return launch_cols_kr11(P, KC, NT, fwd, st);
-        case 12: return launch_cols_kr12(P, KC, NT, fwd, st);
+        case 4: return launch_cols_kr4(P, KC, NT, fwd, st, tma);
+        case 5: return launch_cols_kr5(P, KC, NT, fwd, st, tma);
+        case 6: return launch_cols_kr6(P, KC, NT, fwd, st, tma);
+        case 7: return launch_cols_kr7(P, KC, NT, fwd, st, tma);
+        case 8: return launch_cols_kr8(P, KC, NT, fwd, st, tma);
+        case 9: return launch_cols_kr9(P, KC, NT, fwd, st, tma);
+        case 10: return launch_cols_kr10(P, KC, NT, fwd, st, tma);
+        case 11: return launch_cols_kr11(P, KC, NT, fwd, st, tma);
+        case 12: return launch_cols_kr12(P, KC, NT, fwd, st, tma);
         default: return cudaErrorInvalidValue;
     }
+}
+
+// Tensor maps for the TMA forward column pass ({C, z/C, batch} per operand);
+// ok = 0 when the operands do not fit the bulk-tensor constraints.
+static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+static ColTma make_col_tma(const u32 *a, long long lda, long long z1, const u32 *b, long long ldb,
+                          long long z2, long long batch, int KC, int KR) {
+    ColTma M;
+    memset(&M, 0, sizeof(M));
+    static const bool off = [] { const char *e = getenv("MC_NO_COL_TMA"); return e && *e; }();
+    const long long C = 1ll << KC;
+    const int TC = 16384 >> KR;
+    const int BR = std::min(1 << KR, 256);
+    auto enc = tensor_map_encoder();
+    if (off || !enc || KR < 6 || (z1 % C) || (z2 % C) || (lda % 4) || (ldb % 4) ||
+        ((uintptr_t)a % 16) || ((uintptr_t)b % 16) || batch > 0x7fffffff)
+        return M;
+    auto one = [&](CUtensorMap *m, const u32 *base, long long ld, long long z) {
+        cuuint64_t dims[3] = {(cuuint64_t)C, (cuuint64_t)(z / C), (cuuint64_t)batch};
+        cuuint64_t strides[2] = {(cuuint64_t)C * 4, (cuuint64_t)ld * 4};
+        cuuint32_t box[3] = {(cuuint32_t)TC, (cuuint32_t)BR, 1};
+        cuuint32_t es[3] = {1, 1, 1};
+        return enc(m, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, (void *)base, dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    M.ok = one(&M.ma, a, lda, z1) && one(&M.mb, b, ldb, z2);
+    return M;
 }
 
 static cudaError_t launch_rows_any(int KC, int KR, const FourParams &P, cudaStream_t st) {
@@ -284,11 +327,12 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     MC_CUDA_CHECK(cudaMallocAsync(&scratch, sizeof(u32) * 2 * L * chunk, st));
     P.Ah = scratch;
     P.Bh = scratch + L * chunk;
+    const ColTma tma = make_col_tma(a, lda, P.z1, b, ldb, P.z2, batch, KC, KR);
     mc_status result = MC_OK;
     for (long long p0 = 0; p0 < batch && result == MC_OK; p0 += chunk) {
         P.prod0 = p0;
         P.chunk = (int)std::min(chunk, batch - p0);
-        cudaError_t e = launch_cols_any(KC, KR, NT, P, true, st);
+        cudaError_t e = launch_cols_any(KC, KR, NT, P, true, st, &tma);
         if (e == cudaSuccess) e = launch_rows_any(KC, KR, P, st);
         if (e == cudaSuccess) e = launch_cols_any(KC, KR, NT, P, false, st);
         note_launches(3);

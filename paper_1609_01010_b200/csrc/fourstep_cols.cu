@@ -1,5 +1,7 @@
 // Column passes of the four-step path for one column size KR (compiled once
 // per KR with -DMC_KR=<KR>); see fourstep.cuh for the decomposition.
+#include <algorithm>
+
 #include "fourstep_int.cuh"
 
 #ifndef MC_KR
@@ -95,8 +97,108 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_inv
     }
 }
 
+// Forward column pass, TMA variant: persistent CTAs walk the (product,
+// operand, column tile) list; each tile (R rows x TC columns) arrives by
+// 3-D tensor-map bulk loads into one of two shared buffers while the
+// previous tile is being transformed, so DRAM latency is off the critical
+// path and the 16 strided scalar loads per thread disappear.
 template <int KR, int KC, int NT>
-static cudaError_t launch_one(const FourParams &P, bool fwd, cudaStream_t st) {
+__global__ void __launch_bounds__(1024, 1)
+col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
+                   const __grid_constant__ CUtensorMap tb, int ntiles) {
+    using C = ColCfg<KR>;
+    constexpr int BR = C::R < 256 ? C::R : 256;
+    constexpr int NBOX = C::R / BR;
+    constexpr long long Ccols = 1ll << KC;
+    constexpr int CT = (1 << KC) / C::TC;  // column tiles per operand
+    extern __shared__ __align__(1024) uint4 smem_raw[];
+    uint2 *tf_s = reinterpret_cast<uint2 *>(smem_raw);
+    u32 *buf0 = reinterpret_cast<u32 *>(tf_s + 2 * C::R);
+    u32 *buf1 = buf0 + C::TILE;
+    uint64_t *bar = reinterpret_cast<uint64_t *>(buf1 + C::TILE);
+    for (int i = threadIdx.x; i < C::R / 2; i += C::THREADS)
+        reinterpret_cast<uint4 *>(tf_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_tf) + i);
+    const Tw W{tf_s, tf_s};
+    const int c = threadIdx.x % C::TC;
+    const int t = threadIdx.x / C::TC;
+    const u32 p = P.cs.p;
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        fence_mbar_init();
+    }
+    __syncthreads();
+    auto issue = [&](int tile, int k) {  // thread 0
+        const int ct = tile % CT, op = (tile / CT) & 1, pc = tile / (2 * CT);
+        u32 *dst = k ? buf1 : buf0;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(bar + k, (u32)(C::TILE * 4));
+#pragma unroll
+        for (int bx = 0; bx < NBOX; ++bx)
+            tma_load_3d(dst + bx * BR * C::TC, op ? (const void *)&tb : (const void *)&ta,
+                        ct * C::TC, bx * BR, (int)(P.prod0 + pc), bar + k);
+    };
+    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    uint32_t ph0 = 0, ph1 = 0;
+    int k = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int ct = tile % CT, op = (tile / CT) & 1, pc = tile / (2 * CT);
+        u32 *buf = k ? buf1 : buf0;
+        if (k) {
+            mbar_wait(bar + 1, ph1);
+            ph1 ^= 1;
+        } else {
+            mbar_wait(bar, ph0);
+            ph0 ^= 1;
+        }
+        u32 v[16];
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {  // plain row-major tile: conflict-free for this layout
+            u32 x = buf[(t + C::G * s) * C::TC + c];
+            if (P.reduce) x = mul_shoup(x, 1u, P.red_wp, p);
+            v[s] = x;
+        }
+        __syncthreads();  // tile consumed; the other buffer is free since last iteration
+        if (threadIdx.x == 0 && tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, k ^ 1);
+        const long long z = op ? P.z2 : P.z1;
+        const int zrows = (int)((z + Ccols - 1) / Ccols);
+        fwd_top<KR, NT>(v, zrows, t, P.cs, W);
+        LayCol<C::TC> lay{c};
+        fwd_lower_chain1<KR, 0, LayCol<C::TC>, NT>(buf, v, t, P.cs, W, lay);
+        u32 *dst = (op ? P.Bh : P.Ah) + (long long)pc * (Ccols << KR);
+        const long long col = (long long)ct * C::TC + c;
+        constexpr int SB = last_sb<KR>();
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const int row = slot_pos<SB>(t, s);
+            if (NT >= 16 || (row >> (KR - 4)) < NT) dst[(long long)row * Ccols + col] = v[s];
+        }
+        k ^= 1;
+    }
+}
+
+template <int KR, int KC, int NT>
+static cudaError_t launch_fwd_tma(const FourParams &P, const ColTma &M, cudaStream_t st) {
+    using C = ColCfg<KR>;
+    constexpr int SMEM = 2 * C::R * 8 + 2 * C::TILE * 4 + 64;
+    static bool ready = false;
+    if (!ready) {
+        cudaError_t e = prep_kernel(col_fwd_tma_kernel<KR, KC, NT>, SMEM, C::THREADS, nullptr);
+        if (e != cudaSuccess) return e;
+        ready = true;
+    }
+    const int ntiles = (int)((1ll << KC) / C::TC) * 2 * P.chunk;
+    const int grid = std::min(ntiles, sm_count());
+    col_fwd_tma_kernel<KR, KC, NT><<<grid, C::THREADS, SMEM, st>>>(P, M.ma, M.mb, ntiles);
+    return cudaGetLastError();
+}
+
+template <int KR, int KC, int NT>
+static cudaError_t launch_one(const FourParams &P, bool fwd, cudaStream_t st,
+                              const ColTma *tma) {
+    if constexpr (KR >= 6 && ColCfg<KR>::TILE == 16384) {
+        if (fwd && tma && tma->ok) return launch_fwd_tma<KR, KC, NT>(P, *tma, st);
+    }
     using C = ColCfg<KR>;
     static bool ready_f = false, ready_i = false;  // benign races: idempotent
     dim3 grid((unsigned)((1u << KC) / C::TC), fwd ? 2u : 1u, (unsigned)P.chunk);
@@ -119,16 +221,17 @@ static cudaError_t launch_one(const FourParams &P, bool fwd, cudaStream_t st) {
 }
 
 template <int KR, int KC>
-static cudaError_t launch_nt(const FourParams &P, int NT, bool fwd, cudaStream_t st) {
+static cudaError_t launch_nt(const FourParams &P, int NT, bool fwd, cudaStream_t st,
+                             const ColTma *tma) {
     switch (NT) {
-        case 9: return launch_one<KR, KC, 9>(P, fwd, st);
-        case 10: return launch_one<KR, KC, 10>(P, fwd, st);
-        case 11: return launch_one<KR, KC, 11>(P, fwd, st);
-        case 12: return launch_one<KR, KC, 12>(P, fwd, st);
-        case 13: return launch_one<KR, KC, 13>(P, fwd, st);
-        case 14: return launch_one<KR, KC, 14>(P, fwd, st);
-        case 15: return launch_one<KR, KC, 15>(P, fwd, st);
-        case 16: return launch_one<KR, KC, 16>(P, fwd, st);
+        case 9: return launch_one<KR, KC, 9>(P, fwd, st, tma);
+        case 10: return launch_one<KR, KC, 10>(P, fwd, st, tma);
+        case 11: return launch_one<KR, KC, 11>(P, fwd, st, tma);
+        case 12: return launch_one<KR, KC, 12>(P, fwd, st, tma);
+        case 13: return launch_one<KR, KC, 13>(P, fwd, st, tma);
+        case 14: return launch_one<KR, KC, 14>(P, fwd, st, tma);
+        case 15: return launch_one<KR, KC, 15>(P, fwd, st, tma);
+        case 16: return launch_one<KR, KC, 16>(P, fwd, st, tma);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -137,23 +240,23 @@ static cudaError_t launch_nt(const FourParams &P, int NT, bool fwd, cudaStream_t
 #define MC_CAT(a, b) MC_CAT2(a, b)
 
 cudaError_t MC_CAT(launch_cols_kr, MC_KR)(const FourParams &P, int KC, int NT, bool fwd,
-                                          cudaStream_t st) {
+                                          cudaStream_t st, const ColTma *tma) {
 #if MC_KR == 4
     switch (KC) {  // K = 14, 15, 16
-        case 10: return launch_nt<4, 10>(P, NT, fwd, st);
-        case 11: return launch_nt<4, 11>(P, NT, fwd, st);
-        case 12: return launch_nt<4, 12>(P, NT, fwd, st);
+        case 10: return launch_nt<4, 10>(P, NT, fwd, st, tma);
+        case 11: return launch_nt<4, 11>(P, NT, fwd, st, tma);
+        case 12: return launch_nt<4, 12>(P, NT, fwd, st, tma);
         default: return cudaErrorInvalidValue;
     }
 #elif MC_KR >= 9 && MC_KR <= 11
     switch (KC) {  // K = 21..24 may use 2^13 rows
-        case 12: return launch_nt<MC_KR, 12>(P, NT, fwd, st);
-        case 13: return launch_nt<MC_KR, 13>(P, NT, fwd, st);
+        case 12: return launch_nt<MC_KR, 12>(P, NT, fwd, st, tma);
+        case 13: return launch_nt<MC_KR, 13>(P, NT, fwd, st, tma);
         default: return cudaErrorInvalidValue;
     }
 #else
     if (KC != 12) return cudaErrorInvalidValue;
-    return launch_nt<MC_KR, 12>(P, NT, fwd, st);
+    return launch_nt<MC_KR, 12>(P, NT, fwd, st, tma);
 #endif
 }
 

@@ -2,6 +2,8 @@
 // (fourstep.cu: row pass + orchestration; fourstep_cols.cu: column passes,
 // one unit per column size KR).
 #pragma once
+#include <cuda.h>
+
 #include "conv_small.cuh"
 #include "fourstep.cuh"
 
@@ -71,17 +73,33 @@ struct ColCfg {
     static constexpr int SMEM = 2 * R * 8 + TILE * 4;
 };
 
+// TMA path of the forward column pass: 3-D tensor maps over the operands
+// ({C columns, z/C rows, batch}); rows beyond z/C are zero-filled by TMA.
+struct ColTma {
+    CUtensorMap ma, mb;
+    int ok;  // 0: fall back to the load/store kernel
+};
+
 // Column passes for one KR; NT = active top blocks of the column transform
 // (16 = full; < 16 = truncated: rows >= NT*R/16 are never formed).
-cudaError_t launch_cols_kr4(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
-cudaError_t launch_cols_kr5(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
-cudaError_t launch_cols_kr6(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
-cudaError_t launch_cols_kr7(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
-cudaError_t launch_cols_kr8(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
-cudaError_t launch_cols_kr9(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
-cudaError_t launch_cols_kr10(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
-cudaError_t launch_cols_kr11(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
-cudaError_t launch_cols_kr12(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st);
+cudaError_t launch_cols_kr4(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st,
+                            const ColTma *tma = nullptr);
+cudaError_t launch_cols_kr5(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st,
+                             const ColTma *tma = nullptr);
+cudaError_t launch_cols_kr6(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st,
+                             const ColTma *tma = nullptr);
+cudaError_t launch_cols_kr7(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st,
+                             const ColTma *tma = nullptr);
+cudaError_t launch_cols_kr8(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st,
+                             const ColTma *tma = nullptr);
+cudaError_t launch_cols_kr9(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st,
+                             const ColTma *tma = nullptr);
+cudaError_t launch_cols_kr10(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st,
+                             const ColTma *tma = nullptr);
+cudaError_t launch_cols_kr11(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st,
+                             const ColTma *tma = nullptr);
+cudaError_t launch_cols_kr12(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st,
+                             const ColTma *tma = nullptr);
 
 template <class KF>
 static cudaError_t prep_kernel(KF kern, int smem, int threads, int *per_sm) {
