@@ -69,6 +69,15 @@ def _compile(unit, verbose):
 def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -> str:
     os.makedirs(OBJ, exist_ok=True)
     dep = _deps_mtime()
+    stamp = os.path.join(OBJ, "extra_flags.txt")  # MC_EXTRA_FLAGS of the objects on disk
+    extra_now = os.environ.get("MC_EXTRA_FLAGS", "").strip()
+    try:
+        with open(stamp) as f:
+            force = force or f.read() != extra_now
+    except OSError:
+        force = True
+    with open(stamp, "w") as f:
+        f.write(extra_now)
     todo = []
     units = _units()
     for u in units:

@@ -286,7 +286,10 @@ mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t
         chunk_rows = std::min(chunk_rows, std::max<int64_t>(cap, 1));
     }
     chunk_rows = std::min(chunk_rows, batch);
-    const size_t per_buf = 4ull * chunk_rows * (z1 + z2 + n);
+    // every sub-buffer 256-byte aligned (TMA tensor maps need 16-byte bases)
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t sa = up(4ull * chunk_rows * z1), sb = up(4ull * chunk_rows * z2);
+    const size_t per_buf = sa + sb + up(4ull * chunk_rows * n);
     if (S.bytes < per_buf * PipeState::NBUF) {
         MC_CUDA_CHECK(cudaStreamSynchronize(S.s_out));
         if (S.buf) cudaFree(S.buf);
@@ -301,8 +304,8 @@ mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t
         const int k = (int)(i % PipeState::NBUF);
         const int64_t r0 = i * chunk_rows, rows = std::min(chunk_rows, batch - r0);
         uint32_t *da = (uint32_t *)((char *)S.buf + per_buf * k);
-        uint32_t *db = da + chunk_rows * z1;
-        uint32_t *dc = db + chunk_rows * z2;
+        uint32_t *db = (uint32_t *)((char *)da + sa);
+        uint32_t *dc = (uint32_t *)((char *)db + sb);
         if (i >= PipeState::NBUF) MC_CUDA_CHECK(cudaStreamWaitEvent(S.s_in, S.ev_out[k], 0));
         if (lda == z1)  // contiguous rows: one linear DMA per operand chunk
             MC_CUDA_CHECK(cudaMemcpyAsync(da, a + r0 * lda, 4ull * z1 * rows,

@@ -70,19 +70,26 @@ __device__ __forceinline__ u32 mont_mul(u32 a, u32 b, u32 p, u32 pinv) {
 
 // Decimation-in-frequency butterfly (Gentleman-Sande):
 //   lo = a + b,  hi = (a - b) * w          (transform.py:390-393)
+// Both butterflies are written as plain sums followed by unsigned minima
+// (rather than through add_mod/red1): ptxas then moves about a third of the
+// additions to the FMA pipe as IMAD.IADD, balancing it against the ALU pipe
+// that carries the minima (+7% in the isolated pass benchmark, +3% on
+// config 4; profiles/r01/ubench_pipes.txt).
 __device__ __forceinline__ void bfly_dif(u32 &a, u32 &b, u32 w, u32 wp, u32 p) {
-    u32 s = add_mod(a, b, p);
-    b = mul_shoup(a - b + p, w, wp, p);
-    a = s;
+    const u32 s = a + b;
+    const u32 r = mul_shoup_lazy(a - b + p, w, wp, p);
+    a = min(s, s - p);
+    b = min(r, r - p);
 }
 
 // Decimation-in-time butterfly (Cooley-Tukey):
 //   t = b * w, lo = a + t, hi = a - t      (transform.py:160-163)
 __device__ __forceinline__ void bfly_dit(u32 &a, u32 &b, u32 w, u32 wp, u32 p) {
-    u32 t = mul_shoup(b, w, wp, p);
-    u32 x = a;
-    a = add_mod(x, t, p);
-    b = sub_mod(x, t, p);
+    const u32 r = mul_shoup_lazy(b, w, wp, p);
+    const u32 t = min(r, r - p);
+    const u32 s = a + t, d = a - t + p;
+    a = min(s, s - p);
+    b = min(d, d - p);
 }
 
 }  // namespace mc

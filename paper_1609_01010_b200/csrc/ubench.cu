@@ -40,10 +40,35 @@ __global__ void __launch_bounds__(256) ubench_kernel(u32 *out, u32 seed, int ite
     if (acc == 0x12345678u) out[0] = acc;  // keep the work live
 }
 
+// Butterfly variants of the pass benchmark (MODE):
+//   0  bfly_dif as shipped (canonical values, two VIADDMNMX)
+//   1  canonical, conditional subtractions as IADD3 + IMNMX (ALU pipe)
+//   2  lazy (Harvey): values in [0, 2p), one VIADDMNMX; needs p < 2^30
+//   3  lazy, its reduction as IADD3 + IMNMX
+template <int MODE>
+__device__ __forceinline__ void bfly_variant(u32 &a, u32 &b, u32 w, u32 wp, u32 p) {
+    if (MODE == 0) {
+        bfly_dif(a, b, w, wp, p);
+    } else if (MODE == 1) {
+        const u32 s = a + b, d = a - b + p;
+        const u32 r = mul_shoup_lazy(d, w, wp, p);
+        a = min(s, s - p);
+        b = min(r, r - p);
+    } else if (MODE == 2) {
+        const u32 s = __viaddmin_u32(a, b, a + b - 2 * p);
+        b = mul_shoup_lazy(a - b + 2 * p, w, wp, p);
+        a = s;
+    } else {
+        const u32 s = a + b;
+        b = mul_shoup_lazy(a - b + 2 * p, w, wp, p);
+        a = min(s, s - 2 * p);
+    }
+}
+
 // A radix-16 DIF register pass on two operands (32 butterflies each, one
 // LDS.64 twiddle per butterfly) repeated `iters` times with no exchange and
 // no barrier: the butterfly stream of conv_small_kernel in isolation.
-template <int MINB>
+template <int MINB, int MODE>
 __global__ void __launch_bounds__(256, MINB) pass_bench_kernel(const uint2 *tw_g, u32 *out,
                                                                 int iters, u32 p) {
     __shared__ uint2 tw[4096];
@@ -64,8 +89,8 @@ __global__ void __launch_bounds__(256, MINB) pass_bench_kernel(const uint2 *tw_g
             for (int s = 0; s < 16; ++s) {
                 if (s & H) continue;
                 const uint2 w = tw[(H * 256 + t + 16 * (s & (2 * H - 1))) & 4095];
-                bfly_dif(va[s], va[s + H], w.x, w.y, p);
-                bfly_dif(vb[s], vb[s + H], w.x, w.y, p);
+                bfly_variant<MODE>(va[s], va[s + H], w.x, w.y, p);
+                bfly_variant<MODE>(vb[s], vb[s + H], w.x, w.y, p);
             }
         }
     }
@@ -79,14 +104,15 @@ __global__ void __launch_bounds__(256, MINB) pass_bench_kernel(const uint2 *tw_g
 
 extern "C" {
 
-// Butterflies per clock per SM of the isolated register pass, at 2 and 4
-// resident 256-thread CTAs per SM (rates[0], rates[1]).
+// Butterflies per clock per SM of the isolated register pass:
+// rates[0] MODE 0 at 2 CTAs/SM, rates[1] MODE 0 at 4 CTAs/SM,
+// rates[2..4] MODES 1..3 at 2 CTAs/SM (see bfly_variant).
 mc_status mc_ubench_pass(double *rates) {
     using namespace mc;
     const int sms = sm_count();
     int dev = current_device(), clk_khz = 0;
     cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
-    const u32 p = 2013265921u;
+    const u32 p = 998244353u;  // < 2^30: valid for the lazy modes too
     uint2 *tw = nullptr;
     u32 *out = nullptr;
     MC_CUDA_CHECK(cudaMalloc(&tw, 4096 * sizeof(uint2)));
@@ -103,13 +129,18 @@ mc_status mc_ubench_pass(double *rates) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int iters = 200;
-    for (int k = 0; k < 2; ++k) {
-        const int per_sm = k == 0 ? 2 : 4;
+    for (int k = 0; k < 5; ++k) {
+        const int per_sm = k == 1 ? 4 : 2;
         const int blocks = sms * per_sm;
         for (int rep = 0; rep < 2; ++rep) {
             cudaEventRecord(e0);
-            if (k == 0) pass_bench_kernel<2><<<blocks, 256>>>(tw, out, iters, p);
-            else pass_bench_kernel<4><<<blocks, 256>>>(tw, out, iters, p);
+            switch (k) {
+                case 0: pass_bench_kernel<2, 0><<<blocks, 256>>>(tw, out, iters, p); break;
+                case 1: pass_bench_kernel<4, 0><<<blocks, 256>>>(tw, out, iters, p); break;
+                case 2: pass_bench_kernel<2, 1><<<blocks, 256>>>(tw, out, iters, p); break;
+                case 3: pass_bench_kernel<2, 2><<<blocks, 256>>>(tw, out, iters, p); break;
+                case 4: pass_bench_kernel<2, 3><<<blocks, 256>>>(tw, out, iters, p); break;
+            }
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
         }
