@@ -9,10 +9,10 @@
 
 namespace mc {
 
-template <int NT>
+template <int NT, bool LZ = false>
 static cudaError_t launch_nt(const ConvSmallParams &P, cudaStream_t st) {
     using C = SmallCfg<MC_K>;
-    auto kern = conv_small_kernel<MC_K, NT>;
+    auto kern = conv_small_kernel<MC_K, NT, LZ>;
     // dynamic shared memory: tables + data (+ TMA staging of both rows)
     const int smem = C::SMEM + (P.tma ? 16 + 4 * (P.za16 + P.zb16) : 0);
     static int attr_smem = 0, per_sm = 0, per_sm_smem = -1;  // benign races: idempotent
@@ -50,7 +50,7 @@ cudaError_t MC_CAT(launch_conv_small_k, MC_K)(const ConvSmallParams &P, int nt, 
         case 13: return launch_nt<13>(P, st);
         case 14: return launch_nt<14>(P, st);
         case 15: return launch_nt<15>(P, st);
-        case 16: return launch_nt<16>(P, st);
+        case 16: return P.lazy ? launch_nt<16, true>(P, st) : launch_nt<16>(P, st);
         default: return cudaErrorInvalidValue;
     }
 }

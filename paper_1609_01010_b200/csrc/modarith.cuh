@@ -92,4 +92,85 @@ __device__ __forceinline__ void bfly_dit(u32 &a, u32 &b, u32 w, u32 wp, u32 p) {
     b = min(d, d - p);
 }
 
+// ---------------------------------------------------------------- lazy ranges
+// For p < 2^30 (p1, p2; 4p < 2^32) the transforms keep Harvey's lazy ranges:
+// forward DIF values in [0, 2p), inverse DIT values in [0, 4p).  A DIF
+// butterfly then costs 6 instructions instead of 7 and a DIT butterfly 6
+// instead of 8 (profiles/r01/ubench_pipes.txt).  The Montgomery pointwise
+// product accepts [0, 2p) operands when 4p < 2^32 and returns a canonical
+// residue; kernels canonicalise ([0, 4p) -> [0, p)) before every store of a
+// final result.  LZ = false gives the canonical versions above.
+template <bool LZ>
+__device__ __forceinline__ u32 mul_t(u32 x, u32 w, u32 wp, u32 p) {
+    const u32 r = mul_shoup_lazy(x, w, wp, p);
+    return LZ ? r : min(r, r - p);
+}
+
+template <bool LZ>
+__device__ __forceinline__ u32 mul_t(u32 x, Shoup s, u32 p) { return mul_t<LZ>(x, s.w, s.wp, p); }
+
+// a + b of two forward-range values (LZ: [0,2p) each -> [0,2p))
+template <bool LZ>
+__device__ __forceinline__ u32 add_t(u32 a, u32 b, u32 p) {
+    const u32 s = a + b, q = LZ ? 2 * p : p;
+    return min(s, s - q);
+}
+
+template <bool LZ>
+__device__ __forceinline__ void bfly_dif_t(u32 &a, u32 &b, u32 w, u32 wp, u32 p) {
+    if constexpr (LZ) {
+        const u32 s = a + b;
+        b = mul_shoup_lazy(a - b + 2 * p, w, wp, p);
+        a = min(s, s - 2 * p);
+    } else {
+        bfly_dif(a, b, w, wp, p);
+    }
+}
+
+// DIF butterfly with w = 1
+template <bool LZ>
+__device__ __forceinline__ void bfly_dif1_t(u32 &a, u32 &b, u32 p) {
+    const u32 q = LZ ? 2 * p : p;
+    const u32 s = a + b, d = a - b + q;
+    a = min(s, s - q);
+    b = min(d, d - q);
+}
+
+template <bool LZ>
+__device__ __forceinline__ void bfly_dit_t(u32 &a, u32 &b, u32 w, u32 wp, u32 p) {
+    if constexpr (LZ) {
+        const u32 x = min(a, a - 2 * p);
+        const u32 t = mul_shoup_lazy(b, w, wp, p);
+        a = x + t;
+        b = x - t + 2 * p;
+    } else {
+        bfly_dit(a, b, w, wp, p);
+    }
+}
+
+// DIT butterfly with w = 1
+template <bool LZ>
+__device__ __forceinline__ void bfly_dit1_t(u32 &a, u32 &b, u32 p) {
+    if constexpr (LZ) {
+        const u32 x = min(a, a - 2 * p), y = min(b, b - 2 * p);
+        a = x + y;
+        b = x - y + 2 * p;
+    } else {
+        const u32 s = a + b, d = a - b + p;
+        a = min(s, s - p);
+        b = min(d, d - p);
+    }
+}
+
+// inverse-range value -> canonical residue (identity when !LZ)
+template <bool LZ>
+__device__ __forceinline__ u32 canon_t(u32 x, u32 p) {
+    if constexpr (LZ) {
+        x = min(x, x - 2 * p);
+        return min(x, x - p);
+    } else {
+        return x;
+    }
+}
+
 }  // namespace mc

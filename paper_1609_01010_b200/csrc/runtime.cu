@@ -1,4 +1,5 @@
 // Host runtime: field arithmetic, twiddle-table cache, error state.
+#include <cstdlib>
 #include <atomic>
 #include <cstring>
 #include <map>
@@ -144,6 +145,11 @@ int current_device() {
 
 // Keep stream-ordered scratch (cudaMallocAsync) in the device's default pool
 // across synchronizations instead of unmapping it each time.
+bool lazy_ok(uint32_t p) {
+    static const bool off = [] { const char *e = getenv("MC_NO_LAZY"); return e && *e; }();
+    return !off && p < (1u << 30);
+}
+
 void keep_pool_memory() {
     static bool done[64] = {false};
     const int d = current_device();

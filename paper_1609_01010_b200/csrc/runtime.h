@@ -65,6 +65,9 @@ mc_status get_tables(u32 p, int log2L, const FieldTables **out);
 
 int current_device();
 void keep_pool_memory();
+// Lazy-range arithmetic (modarith.cuh) is valid for p < 2^30; MC_NO_LAZY
+// (non-empty) forces the canonical kernels for A/B runs.
+bool lazy_ok(uint32_t p);
 int sm_count();
 
 }  // namespace mc

@@ -18,7 +18,7 @@ if torch.cuda.is_available():
 
 
 @pytest.mark.parametrize("K", [14, 15, 16, 17, 18])
-@pytest.mark.parametrize("p", [P2, P3])
+@pytest.mark.parametrize("p", [P1, P2, P3])
 def test_fourstep_sizes_vs_oracle(orc, K, p):
     L = 1 << K
     for n in sorted({L, L - 1, L // 2 + 1, (3 * L) // 4 + 5}):
