@@ -1,6 +1,7 @@
 // Column passes of the four-step path for one column size KR (compiled once
 // per KR with -DMC_KR=<KR>); see fourstep.cuh for the decomposition.
 #include <algorithm>
+#include <cstdlib>
 
 #include "fourstep_int.cuh"
 
@@ -178,6 +179,108 @@ col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
     }
 }
 
+// Inverse column pass, async-copy variant: persistent CTAs; the next tile's
+// rows arrive by 16-byte cp.async (LDGSTS.128, 4 per thread instead of 16
+// scalar loads) into the other of two shared buffers while this tile is
+// transformed.  Landing layout: row r at r*TC + (r/16)*8 words, which makes
+// the first read (rows 16t + s, the last forward pass's layout) conflict-free.
+template <int KR>
+struct ColInvAsync {
+    static constexpr int PADW = 8;  // words of padding per 16 rows
+    static constexpr int BUFW = ColCfg<KR>::TILE + (ColCfg<KR>::R / 16) * PADW;
+    static constexpr int SMEM = 2 * ColCfg<KR>::R * 8 + 2 * BUFW * 4;
+    __device__ static __forceinline__ int off(int row) {
+        return row * ColCfg<KR>::TC + (row >> 4) * PADW;
+    }
+};
+
+template <int KR, int KC, int NT, bool LZ>
+__global__ void __launch_bounds__(1024, 1) col_inv_async_kernel(const FourParams P, int ntiles) {
+    using C = ColCfg<KR>;
+    using A = ColInvAsync<KR>;
+    constexpr long long Ccols = 1ll << KC;
+    constexpr int CT = (1 << KC) / C::TC;
+    constexpr int CHUNKS = C::TC / 4;     // 16-byte chunks per row
+    constexpr int NR = NT * (C::R / 16);  // rows of the column spectrum that were formed
+    extern __shared__ __align__(1024) uint4 smem_raw[];
+    uint2 *tf_s = reinterpret_cast<uint2 *>(smem_raw);
+    uint2 *ti_s = tf_s + C::R;
+    u32 *bufs = reinterpret_cast<u32 *>(tf_s + 2 * C::R);
+    for (int i = threadIdx.x; i < C::R / 2; i += C::THREADS) {
+        reinterpret_cast<uint4 *>(ti_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_ti) + i);
+        if (NT < 16)
+            reinterpret_cast<uint4 *>(tf_s)[i] =
+                __ldg(reinterpret_cast<const uint4 *>(P.col_tf) + i);
+    }
+    const Tw W{tf_s, ti_s};
+    const int c = threadIdx.x % C::TC;
+    const int t = threadIdx.x / C::TC;
+    auto issue = [&](int tile, int k) {  // every thread: its share of the tile's chunks
+        const int ct = tile % CT, pc = tile / CT;
+        const u32 *src = P.Ah + (long long)pc * (Ccols << KR) + (long long)ct * C::TC;
+        u32 *dst = bufs + k * A::BUFW;
+        for (int q = threadIdx.x; q < NR * CHUNKS; q += C::THREADS) {
+            const int row = q / CHUNKS, ch = q % CHUNKS;
+            const u32 *g = src + (long long)row * Ccols + 4 * ch;
+            const u32 sa = smem_u32(dst + A::off(row) + 4 * ch);
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(g) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    int k = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int ct = tile % CT, pc = tile / CT;
+        u32 *buf = bufs + k * A::BUFW;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncthreads();
+        u32 v[16];
+        constexpr int SB = last_sb<KR>();
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const int row = slot_pos<SB>(t, s);
+            v[s] = (NT >= 16 || (row >> (KR - 4)) < NT) ? buf[A::off(row) + c] : 0u;
+        }
+        __syncthreads();  // tile consumed; the other buffer is free
+        if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, k ^ 1);
+        LayCol<C::TC> lay{c};
+        inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, NT, LZ>(buf, v, t, P.cs, W, lay);
+        ItftTop<KR, 16, NT, 0, LZ>::run(v, t, P.cs, W);
+        u32 *dst = P.c + (P.prod0 + pc) * P.ldc;
+        const long long col = (long long)ct * C::TC + c;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            const long long idx = (long long)(t + C::G * s) * Ccols + col;
+            if (idx < P.n) __stcs(dst + idx, canon_t<LZ>(v[s], P.cs.p));
+        }
+        k ^= 1;
+    }
+}
+
+template <int KR, int KC, int NT, bool LZ>
+static cudaError_t launch_inv_async(const FourParams &P, cudaStream_t st) {
+    using C = ColCfg<KR>;
+    static bool ready = false;
+    if (!ready) {
+        cudaError_t e = prep_kernel(col_inv_async_kernel<KR, KC, NT, LZ>, ColInvAsync<KR>::SMEM,
+                                    C::THREADS, nullptr);
+        if (e != cudaSuccess) return e;
+        ready = true;
+    }
+    const int ntiles = (int)((1ll << KC) / C::TC) * P.chunk;
+    const int grid = std::min(ntiles, sm_count());
+    col_inv_async_kernel<KR, KC, NT, LZ>
+        <<<grid, C::THREADS, ColInvAsync<KR>::SMEM, st>>>(P, ntiles);
+    return cudaGetLastError();
+}
+
+// On by default (+1% on configs 4 and 5: the pass is bound by its instruction
+// stream, not by the load latency this hides); MC_NO_COL_INV_ASYNC disables.
+static bool col_inv_async_on() {
+    static const bool on = [] { const char *e = getenv("MC_NO_COL_INV_ASYNC"); return !(e && *e); }();
+    return on;
+}
+
 template <int KR, int KC, int NT, bool LZ>
 static cudaError_t launch_fwd_tma(const FourParams &P, const ColTma &M, cudaStream_t st) {
     using C = ColCfg<KR>;
@@ -199,6 +302,7 @@ static cudaError_t launch_one(const FourParams &P, bool fwd, cudaStream_t st,
                               const ColTma *tma) {
     if constexpr (KR >= 6 && ColCfg<KR>::TILE == 16384) {
         if (fwd && tma && tma->ok) return launch_fwd_tma<KR, KC, NT, LZ>(P, *tma, st);
+        if (!fwd && col_inv_async_on()) return launch_inv_async<KR, KC, NT, LZ>(P, st);
     }
     using C = ColCfg<KR>;
     static bool ready_f = false, ready_i = false;  // benign races: idempotent
