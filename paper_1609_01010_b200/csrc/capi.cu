@@ -147,7 +147,7 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
         }
         if (batch > 0x7fffffffll * SmallCfg<4>::PPC)
             return fail(MC_EINVAL, "batch too large for one launch");
-        P.lazy = (nt == 16 && lazy_ok(p)) ? 1 : 0;
+        P.ar = (nt == 16 && lazy_ok(p)) ? 1 : 2;
         cudaError_t e = launch_small(K, P, nt, st);
         note_launches(1);
         if (e != cudaSuccess) return cuda_fail(e, "conv_small launch");

@@ -60,7 +60,7 @@ struct ConvSmallParams {
     int za16, zb16;    // words of a / b rows covered by the bulk copies (multiple of 4)
     uint2 c16f[16];    // tf[1..15] / ti[1..15]: the thread-invariant twiddles of the
     uint2 c16i[16];    // lowest pass (h <= 8), read from the constant bank
-    int lazy;          // complete transforms with p < 2^30: the lazy-range (LZ) variant
+    int ar;            // arithmetic mode of the launch (modarith.cuh): 1 or 2
 };
 
 // 32-bank conflict-free swizzle for the three access patterns used here:
@@ -92,7 +92,7 @@ struct Tw {
 // zeros are real zeros in the registers, so the result is exact).  No
 // runtime branch splits the unrolled butterflies, so ptxas can interleave
 // the independent chains.
-template <int K, int NT, int ZS, bool LZ = false>
+template <int K, int NT, int ZS, int AR = 0>
 __device__ __forceinline__ void fwd_top_zs(u32 (&v)[16], int t, const ConvSmallParams &P,
                                            const Tw &W) {
     constexpr int G = 1 << (K - 4);
@@ -113,13 +113,13 @@ __device__ __forceinline__ void fwd_top_zs(u32 (&v)[16], int t, const ConvSmallP
             if (!hi_zero) {
                 if (hi_needed) {
                     const uint2 w = ldtw(W.tf, h + t + G * so);
-                    bfly_dif_t<LZ>(v[s], v[s + H], w.x, w.y, p);
+                    bfly_dif_t<AR>(v[s], v[s + H], w.x, w.y, p);
                 } else {
-                    v[s] = add_t<LZ>(v[s], v[s + H], p);  // lo-only add (fold)
+                    v[s] = add_t<AR>(v[s], v[s + H], p);  // lo-only add (fold)
                 }
             } else if (hi_needed) {
                 const uint2 w = ldtw(W.tf, h + t + G * so);
-                v[s + H] = mul_t<LZ>(v[s], w.x, w.y, p);  // hi input is zero
+                v[s + H] = mul_t<AR>(v[s], w.x, w.y, p);  // hi input is zero
             }
         }
     }
@@ -131,33 +131,33 @@ __device__ __forceinline__ void fwd_top_zs(u32 (&v)[16], int t, const ConvSmallP
 #define MC_ZS_STEP 4
 #endif
 
-template <int K, int NT, bool LZ = false>
+template <int K, int NT, int AR = 0>
 __device__ __forceinline__ void fwd_top(u32 (&v)[16], int z, int t, const ConvSmallParams &P,
                                         const Tw &W) {
     constexpr int G = 1 << (K - 4);
     const int zs = (z + G - 1) / G;  // uniform across the launch
 #if MC_ZS_STEP == 2
-    if (zs <= 2) fwd_top_zs<K, NT, 2, LZ>(v, t, P, W);
-    else if (zs <= 4) fwd_top_zs<K, NT, 4, LZ>(v, t, P, W);
-    else if (zs <= 6) fwd_top_zs<K, NT, 6, LZ>(v, t, P, W);
-    else if (zs <= 8) fwd_top_zs<K, NT, 8, LZ>(v, t, P, W);
-    else if (zs <= 10) fwd_top_zs<K, NT, 10, LZ>(v, t, P, W);
-    else if (zs <= 12) fwd_top_zs<K, NT, 12, LZ>(v, t, P, W);
-    else if (zs <= 14) fwd_top_zs<K, NT, 14, LZ>(v, t, P, W);
-    else fwd_top_zs<K, NT, 16, LZ>(v, t, P, W);
+    if (zs <= 2) fwd_top_zs<K, NT, 2, AR>(v, t, P, W);
+    else if (zs <= 4) fwd_top_zs<K, NT, 4, AR>(v, t, P, W);
+    else if (zs <= 6) fwd_top_zs<K, NT, 6, AR>(v, t, P, W);
+    else if (zs <= 8) fwd_top_zs<K, NT, 8, AR>(v, t, P, W);
+    else if (zs <= 10) fwd_top_zs<K, NT, 10, AR>(v, t, P, W);
+    else if (zs <= 12) fwd_top_zs<K, NT, 12, AR>(v, t, P, W);
+    else if (zs <= 14) fwd_top_zs<K, NT, 14, AR>(v, t, P, W);
+    else fwd_top_zs<K, NT, 16, AR>(v, t, P, W);
 #elif MC_ZS_STEP == 4
-    if (zs <= 4) fwd_top_zs<K, NT, 4, LZ>(v, t, P, W);
-    else if (zs <= 8) fwd_top_zs<K, NT, 8, LZ>(v, t, P, W);
-    else if (zs <= 12) fwd_top_zs<K, NT, 12, LZ>(v, t, P, W);
-    else fwd_top_zs<K, NT, 16, LZ>(v, t, P, W);
+    if (zs <= 4) fwd_top_zs<K, NT, 4, AR>(v, t, P, W);
+    else if (zs <= 8) fwd_top_zs<K, NT, 8, AR>(v, t, P, W);
+    else if (zs <= 12) fwd_top_zs<K, NT, 12, AR>(v, t, P, W);
+    else fwd_top_zs<K, NT, 16, AR>(v, t, P, W);
 #else
-    if (zs <= 8) fwd_top_zs<K, NT, 8, LZ>(v, t, P, W);
-    else fwd_top_zs<K, NT, 16, LZ>(v, t, P, W);
+    if (zs <= 8) fwd_top_zs<K, NT, 8, AR>(v, t, P, W);
+    else fwd_top_zs<K, NT, 16, AR>(v, t, P, W);
 #endif
 }
 
 // ---------------------------------------------------------------- lower passes
-template <int K, int LO, int HI, int SB, bool LZ = false>
+template <int K, int LO, int HI, int SB, int AR = 0>
 __device__ __forceinline__ void fwd_lower(u32 (&v)[16], int t, const ConvSmallParams &P,
                                           const Tw &W) {
     const u32 p = P.p;
@@ -172,21 +172,21 @@ __device__ __forceinline__ void fwd_lower(u32 (&v)[16], int t, const ConvSmallPa
             if (SB == 0) {  // twiddle index is compile-time: w_{2h}^(s mod h)
                 const int j = s & (h - 1);
                 if (j == 0) {  // w = 1: no multiplication
-                    bfly_dif1_t<LZ>(v[s], v[s | (1 << sbit)], p);
+                    bfly_dif1_t<AR>(v[s], v[s | (1 << sbit)], p);
                 } else {
                     const uint2 w = P.c16f[h + j];
-                    bfly_dif_t<LZ>(v[s], v[s | (1 << sbit)], w.x, w.y, p);
+                    bfly_dif_t<AR>(v[s], v[s | (1 << sbit)], w.x, w.y, p);
                 }
                 continue;
             }
             const int j = (tpos | (s << SB)) & (h - 1);
             const uint2 w = ldtw(W.tf, h + j);
-            bfly_dif_t<LZ>(v[s], v[s | (1 << sbit)], w.x, w.y, p);
+            bfly_dif_t<AR>(v[s], v[s | (1 << sbit)], w.x, w.y, p);
         }
     }
 }
 
-template <int K, int LO, int HI, int SB, bool LZ = false>
+template <int K, int LO, int HI, int SB, int AR = 0>
 __device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallParams &P,
                                           const Tw &W) {
     const u32 p = P.p;
@@ -201,27 +201,27 @@ __device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallPa
             if (SB == 0) {
                 const int j = s & (h - 1);
                 if (j == 0) {  // w = 1
-                    bfly_dit1_t<LZ>(v[s], v[s | (1 << sbit)], p);
+                    bfly_dit1_t<AR>(v[s], v[s | (1 << sbit)], p);
                 } else {
                     const uint2 w = P.c16i[h + j];
-                    bfly_dit_t<LZ>(v[s], v[s | (1 << sbit)], w.x, w.y, p);
+                    bfly_dit_t<AR>(v[s], v[s | (1 << sbit)], w.x, w.y, p);
                 }
                 continue;
             }
             const int j = (tpos | (s << SB)) & (h - 1);
             const uint2 w = ldtw(W.ti, h + j);
-            bfly_dit_t<LZ>(v[s], v[s | (1 << sbit)], w.x, w.y, p);
+            bfly_dit_t<AR>(v[s], v[s | (1 << sbit)], w.x, w.y, p);
         }
     }
 }
 
 // ---------------------------------------------------------------- top pass (inverse)
 // transform.py:451-489 restricted to slot granularity.  M, N, OFF in slots;
-// level index LV = log2 M (m = M*G elements).  LZ (lazy ranges) only for the
-// complete transform (N == M), which is a plain DIT.
-template <int K, int M, int N, int OFF, bool LZ = false>
+// level index LV = log2 M (m = M*G elements).  Lazy modes (AR != 0) only for
+// the complete transform (N == M), which is a plain DIT.
+template <int K, int M, int N, int OFF, int AR = 0>
 struct ItftTop {
-    static_assert(!LZ || N == M || N == 0, "lazy ranges only on the complete inverse");
+    static_assert(AR == 0 || N == M || N == 0, "lazy ranges only on the complete inverse");
     static __device__ __forceinline__ void run(u32 (&v)[16], int t, const ConvSmallParams &P,
                                                const Tw &W) {
         constexpr int G = 1 << (K - 4);
@@ -243,7 +243,7 @@ struct ItftTop {
                 v[OFF + s] = sub_mod(add_mod(a, a, p), mul_shoup(v[OFF + s + H], mm, p), p);
             }
         } else {
-            ItftTop<K, H, H, OFF, LZ>::run(v, t, P, W);  // complete first half
+            ItftTop<K, H, H, OFF, AR>::run(v, t, P, W);  // complete first half
             const Shoup mm = P.mlev[LV];
             const Shoup ih = P.hinv[LV];
             constexpr int h = H * G;
@@ -255,15 +255,29 @@ struct ItftTop {
                 v[OFF + s + H] = mul_shoup(d, w.x, w.y, p);
                 v[OFF + s] = sub_mod(add_mod(a, a, p), mul_shoup(b, mm, p), p);
             }
-            ItftTop<K, H, N - H, OFF + H, LZ>::run(v, t, P, W);
+            ItftTop<K, H, N - H, OFF + H, AR>::run(v, t, P, W);
 #pragma unroll
             for (int s = 0; s < N - H; ++s) {  // inverse DIT butterflies
                 const uint2 w = ldtw(W.ti, h + t + G * s);
-                bfly_dit_t<LZ>(v[OFF + s], v[OFF + s + H], w.x, w.y, p);
+                bfly_dit_t<AR>(v[OFF + s], v[OFF + s + H], w.x, w.y, p);
             }
         }
     }
 };
+
+// Inverse top pass in mode AR; the truncated recursion (NT < 16) runs on
+// canonical residues, so lazy values are canonicalised first.
+template <int K, int NT, int AR>
+__device__ __forceinline__ void inv_top(u32 (&v)[16], int t, const ConvSmallParams &P,
+                                        const Tw &W) {
+    if constexpr (NT < 16 && AR != 0) {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) v[s] = canon_t<AR>(v[s], P.p);
+        ItftTop<K, 16, NT, 0, 0>::run(v, t, P, W);
+    } else {
+        ItftTop<K, 16, NT, 0, AR>::run(v, t, P, W);
+    }
+}
 
 // ---------------------------------------------------------------- exchange
 // Shared-memory address of transform position x.  LaySmall: one transform
@@ -336,7 +350,7 @@ __device__ __forceinline__ bool pass_active(int t) {
     else return gblock_of_pass<K, I>(t & ~31) < NT;  // warp-uniform
 }
 
-template <int K, int NT, int I, bool LZ = false>
+template <int K, int NT, int I, int AR = 0>
 __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[16], u32 (&vb)[16],
                                                 int t, const ConvSmallParams &P, const Tw &W) {
     if constexpr (I < Plan<K>::NP) {
@@ -351,34 +365,34 @@ __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[
         // Inactive G-blocks (>= NT) are skipped per warp where possible;
         // otherwise transformed and discarded at the pointwise step.
         if (pass_active<K, I, NT>(t)) {
-            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, LZ>(va, t, P, W);
-            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, LZ>(vb, t, P, W);
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR>(va, t, P, W);
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR>(vb, t, P, W);
         }
-        fwd_lower_chain<K, NT, I + 1, LZ>(bufA, bufB, va, vb, t, P, W);
+        fwd_lower_chain<K, NT, I + 1, AR>(bufA, bufB, va, vb, t, P, W);
     }
 }
 
 // Inverse lower passes in reverse order (lowest bits first); on exit the
 // slots are in the top-pass layout.
-template <int K, int NT, int I, bool LZ = false>
+template <int K, int NT, int I, int AR = 0>
 __device__ __forceinline__ void inv_lower_chain(u32 *buf, u32 (&v)[16], int t,
                                                 const ConvSmallParams &P, const Tw &W) {
     if constexpr (I >= 0) {
         constexpr int SB = Plan<K>::sb(I);
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         if (pass_active<K, I, NT>(t))
-            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, LZ>(v, t, P, W);  // zeros stay zeros
+            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR>(v, t, P, W);  // zeros stay zeros
         __syncthreads();
         put<SB>(buf, v, t);
         __syncthreads();
         get<SBnext>(buf, v, t);
-        inv_lower_chain<K, NT, I - 1, LZ>(buf, v, t, P, W);
+        inv_lower_chain<K, NT, I - 1, AR>(buf, v, t, P, W);
     }
 }
 
 // One operand, arbitrary layout: forward lower passes; on exit the slots
 // are in the last lower pass's layout.
-template <int K, int I, class Lay, int NT = 16, bool LZ = false>
+template <int K, int I, class Lay, int NT = 16, int AR = 0>
 __device__ __forceinline__ void fwd_lower_chain1(u32 *buf, u32 (&v)[16], int t,
                                                  const ConvSmallParams &P, const Tw &W, Lay lay) {
     if constexpr (I < Plan<K>::NP) {
@@ -389,24 +403,24 @@ __device__ __forceinline__ void fwd_lower_chain1(u32 *buf, u32 (&v)[16], int t,
         __syncthreads();
         get<SB>(buf, v, t, lay);
         if (NT >= 16 || gblock_of_pass<K, I>(t) < NT)
-            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, LZ>(v, t, P, W);
-        fwd_lower_chain1<K, I + 1, Lay, NT, LZ>(buf, v, t, P, W, lay);
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR>(v, t, P, W);
+        fwd_lower_chain1<K, I + 1, Lay, NT, AR>(buf, v, t, P, W, lay);
     }
 }
 
-template <int K, int I, class Lay, int NT = 16, bool LZ = false>
+template <int K, int I, class Lay, int NT = 16, int AR = 0>
 __device__ __forceinline__ void inv_lower_chain1(u32 *buf, u32 (&v)[16], int t,
                                                  const ConvSmallParams &P, const Tw &W, Lay lay) {
     if constexpr (I >= 0) {
         constexpr int SB = Plan<K>::sb(I);
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         if (NT >= 16 || gblock_of_pass<K, I>(t) < NT)
-            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, LZ>(v, t, P, W);
+            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR>(v, t, P, W);
         __syncthreads();
         put<SB>(buf, v, t, lay);
         __syncthreads();
         get<SBnext>(buf, v, t, lay);
-        inv_lower_chain1<K, I - 1, Lay, NT, LZ>(buf, v, t, P, W, lay);
+        inv_lower_chain1<K, I - 1, Lay, NT, AR>(buf, v, t, P, W, lay);
     }
 }
 
@@ -427,10 +441,10 @@ struct SmallCfg {
 
 // Persistent kernel: each CTA copies the (p, L) stage tables into shared
 // memory once and then walks the batch with a grid stride.
-template <int K, int NT, bool LZ = false>
+template <int K, int NT, int AR = 0>
 __global__ void __launch_bounds__(SmallCfg<K>::THREADS, SmallCfg<K>::MINB)
 conv_small_kernel(const ConvSmallParams P) {
-    static_assert(!LZ || NT == 16, "lazy ranges only for complete transforms");
+    static_assert(AR != 1 || NT == 16, "Harvey ranges only for complete transforms");
     using C = SmallCfg<K>;
     constexpr int L = C::L, T = C::T;
     extern __shared__ uint4 smem_raw[];
@@ -515,14 +529,14 @@ conv_small_kernel(const ConvSmallParams P) {
         if (P.reduce) {  // three-primes inputs: any 32-bit word -> residue
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
-                va[s] = mul_t<LZ>(va[s], 1u, P.red_wp, P.p);
-                vb[s] = mul_t<LZ>(vb[s], 1u, P.red_wp, P.p);
+                va[s] = mul_t<AR>(va[s], 1u, P.red_wp, P.p);
+                vb[s] = mul_t<AR>(vb[s], 1u, P.red_wp, P.p);
             }
         }
 
-        fwd_top<K, NT, LZ>(va, P.z1, t, P, W);
-        fwd_top<K, NT, LZ>(vb, P.z2, t, P, W);
-        fwd_lower_chain<K, NT, 0, LZ>(bufA, bufB, va, vb, t, P, W);
+        fwd_top<K, NT, AR>(va, P.z1, t, P, W);
+        fwd_top<K, NT, AR>(vb, P.z2, t, P, W);
+        fwd_lower_chain<K, NT, 0, AR>(bufA, bufB, va, vb, t, P, W);
 
         // pointwise product in the last pass's layout, L^-1 folded in
         {
@@ -533,7 +547,7 @@ conv_small_kernel(const ConvSmallParams P) {
                 if ((slot_pos<SB>(t, 0) >> (K - 4)) < NT) {
 #pragma unroll
                     for (int s = 0; s < 16; ++s)
-                        va[s] = mul_shoup(mont_mul(va[s], vb[s], P.p, P.pinv), P.linv_mont, P.p);
+                        va[s] = mul_inv_t<AR>(mont_mul(va[s], vb[s], P.p, P.pinv), P.linv_mont, P.p);
                 } else {
 #pragma unroll
                     for (int s = 0; s < 16; ++s) va[s] = 0u;  // inactive tail: u_j = 0
@@ -543,22 +557,22 @@ conv_small_kernel(const ConvSmallParams P) {
                 for (int s = 0; s < 16; ++s) {
                     const int x = slot_pos<SB>(t, s);
                     if (NT >= 16 || (x >> (K - 4)) < NT)
-                        va[s] = mul_t<LZ>(mont_mul(va[s], vb[s], P.p, P.pinv), P.linv_mont, P.p);
+                        va[s] = mul_inv_t<AR>(mont_mul(va[s], vb[s], P.p, P.pinv), P.linv_mont, P.p);
                     else
                         va[s] = 0u;  // time values of the inactive tail: u_j = 0
                 }
             }
         }
 
-        inv_lower_chain<K, NT, Plan<K>::NP - 1, LZ>(bufA, va, t, P, W);
-        ItftTop<K, 16, NT, 0, LZ>::run(va, t, P, W);
+        inv_lower_chain<K, NT, Plan<K>::NP - 1, AR>(bufA, va, t, P, W);
+        inv_top<K, NT, AR>(va, t, P, W);
 
         if (valid) {
             u32 *gc = P.c + row * P.ldc;
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 const int x = (s << (K - 4)) | t;
-                if (x < P.n) __stcs(gc + x, canon_t<LZ>(va[s], P.p));
+                if (x < P.n) __stcs(gc + x, canon_t<(NT < 16 ? 0 : AR)>(va[s], P.p));
             }
         }
     }

@@ -9,10 +9,10 @@
 
 namespace mc {
 
-template <int NT, bool LZ = false>
+template <int NT, int AR>
 static cudaError_t launch_nt(const ConvSmallParams &P, cudaStream_t st) {
     using C = SmallCfg<MC_K>;
-    auto kern = conv_small_kernel<MC_K, NT, LZ>;
+    auto kern = conv_small_kernel<MC_K, NT, AR>;
     // dynamic shared memory: tables + data (+ TMA staging of both rows)
     const int smem = C::SMEM + (P.tma ? 16 + 4 * (P.za16 + P.zb16) : 0);
     static int attr_smem = 0, per_sm = 0, per_sm_smem = -1;  // benign races: idempotent
@@ -43,14 +43,14 @@ static cudaError_t launch_nt(const ConvSmallParams &P, cudaStream_t st) {
 
 cudaError_t MC_CAT(launch_conv_small_k, MC_K)(const ConvSmallParams &P, int nt, cudaStream_t st) {
     switch (nt) {
-        case 9: return launch_nt<9>(P, st);
-        case 10: return launch_nt<10>(P, st);
-        case 11: return launch_nt<11>(P, st);
-        case 12: return launch_nt<12>(P, st);
-        case 13: return launch_nt<13>(P, st);
-        case 14: return launch_nt<14>(P, st);
-        case 15: return launch_nt<15>(P, st);
-        case 16: return P.lazy ? launch_nt<16, true>(P, st) : launch_nt<16>(P, st);
+        case 9: return launch_nt<9, 2>(P, st);
+        case 10: return launch_nt<10, 2>(P, st);
+        case 11: return launch_nt<11, 2>(P, st);
+        case 12: return launch_nt<12, 2>(P, st);
+        case 13: return launch_nt<13, 2>(P, st);
+        case 14: return launch_nt<14, 2>(P, st);
+        case 15: return launch_nt<15, 2>(P, st);
+        case 16: return P.ar == 1 ? launch_nt<16, 1>(P, st) : launch_nt<16, 2>(P, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -21,8 +21,8 @@ struct RowCfg {
     static constexpr int SMEM = 2 * C * 8 + PPC * (2 * C * 4 + 32 * 8);
 };
 
-// LZ: lazy ranges (p < 2^30): inputs and outputs in [0, 2p).
-template <int KC, bool LZ = false>
+// AR: arithmetic mode (modarith.cuh); inputs and outputs in [0, 2p).
+template <int KC, int AR = 0>
 __global__ void __launch_bounds__(RowCfg<KC>::THREADS, RowCfg<KC>::THREADS >= 512 ? 1 : 2)
 row_conv_kernel(const FourParams P, int KR) {
     using RC = RowCfg<KC>;
@@ -78,22 +78,22 @@ row_conv_kernel(const FourParams P, int KR) {
         for (int s = 0; s < 16; ++s) {
             const int x = t + G * s;
             const uint2 bt = beta[s];
-            va[s] = mul_t<LZ>(mul_t<LZ>(valid ? rowA[x] : 0u, af, afp, p), bt.x, bt.y, p);
-            vb[s] = mul_t<LZ>(mul_t<LZ>(valid ? rowB[x] : 0u, af, afp, p), bt.x, bt.y, p);
+            va[s] = mul_t<AR>(mul_t<AR>(valid ? rowA[x] : 0u, af, afp, p), bt.x, bt.y, p);
+            vb[s] = mul_t<AR>(mul_t<AR>(valid ? rowB[x] : 0u, af, afp, p), bt.x, bt.y, p);
         }
-        fwd_top<KC, 16, LZ>(va, Cn, t, P.cs, W);
-        fwd_top<KC, 16, LZ>(vb, Cn, t, P.cs, W);
-        fwd_lower_chain<KC, 16, 0, LZ>(bufA, bufB, va, vb, t, P.cs, W);
+        fwd_top<KC, 16, AR>(va, Cn, t, P.cs, W);
+        fwd_top<KC, 16, AR>(vb, Cn, t, P.cs, W);
+        fwd_lower_chain<KC, 16, 0, AR>(bufA, bufB, va, vb, t, P.cs, W);
 #pragma unroll
         for (int s = 0; s < 16; ++s)
-            va[s] = mul_t<LZ>(mont_mul(va[s], vb[s], p, P.cs.pinv), P.cs.linv_mont, p);
-        inv_lower_chain<KC, 16, Plan<KC>::NP - 1, LZ>(bufA, va, t, P.cs, W);
-        ItftTop<KC, 16, 16, 0, LZ>::run(va, t, P.cs, W);
+            va[s] = mul_inv_t<AR>(mont_mul(va[s], vb[s], p, P.cs.pinv), P.cs.linv_mont, p);
+        inv_lower_chain<KC, 16, Plan<KC>::NP - 1, AR>(bufA, va, t, P.cs, W);
+        ItftTop<KC, 16, 16, 0, AR>::run(va, t, P.cs, W);
         if (valid) {
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 const uint2 bt = beta[16 + s];
-                rowA[t + G * s] = mul_t<LZ>(mul_t<LZ>(va[s], ai, aip, p), bt.x, bt.y, p);
+                rowA[t + G * s] = mul_inv_t<AR>(mul_inv_t<AR>(va[s], ai, aip, p), bt.x, bt.y, p);
             }
         }
         __syncthreads();
@@ -171,23 +171,23 @@ mc_status get_twist_tables(u32 p, int K, const u32 **lo_f, const uint2 **hi_f, c
     return MC_OK;
 }
 
-template <int KC, bool LZ>
+template <int KC, int AR>
 static cudaError_t launch_rows_lz(const FourParams &P, int KR, cudaStream_t st) {
     using RC = RowCfg<KC>;
     static int per_sm = 0;
     if (!per_sm) {
-        cudaError_t e = prep_kernel(row_conv_kernel<KC, LZ>, RC::SMEM, RC::THREADS, &per_sm);
+        cudaError_t e = prep_kernel(row_conv_kernel<KC, AR>, RC::SMEM, RC::THREADS, &per_sm);
         if (e != cudaSuccess) return e;
     }
     long long work = (P.nrows * P.chunk + RC::PPC - 1) / RC::PPC;
     long long grid = std::min<long long>(work, (long long)per_sm * sm_count());
-    row_conv_kernel<KC, LZ><<<(unsigned)grid, RC::THREADS, RC::SMEM, st>>>(P, KR);
+    row_conv_kernel<KC, AR><<<(unsigned)grid, RC::THREADS, RC::SMEM, st>>>(P, KR);
     return cudaGetLastError();
 }
 
 template <int KC>
 static cudaError_t launch_rows(const FourParams &P, int KR, cudaStream_t st) {
-    return P.cs.lazy ? launch_rows_lz<KC, true>(P, KR, st) : launch_rows_lz<KC, false>(P, KR, st);
+    return P.cs.ar == 1 ? launch_rows_lz<KC, 1>(P, KR, st) : launch_rows_lz<KC, 2>(P, KR, st);
 }
 
 static cudaError_t launch_cols_any(int KC, int KR, int NT, const FourParams &P, bool fwd,
@@ -320,7 +320,7 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     int NT = 16;
     if (engine == 1 && !circ) NT = (int)((n + (L >> 4) - 1) / (L >> 4));
     P.nrows = (long long)NT << (KR - 4);
-    P.cs.lazy = (NT == 16 && lazy_ok(p)) ? 1 : 0;
+    P.cs.ar = (NT == 16 && lazy_ok(p)) ? 1 : 2;
     // scratch budget per chunk (default 512 MiB: bigger launches beat L2 residency,
     // the four-step passes are integer-pipe bound; profiles/r01/README.md)
     static const long long budget_words = [] {

@@ -14,8 +14,8 @@ namespace mc {
 // Forward: R-point DIF down each column of a TC-wide tile.  Truncated (NT <
 // 16): top-pass outputs of blocks >= NT are pruned, lower passes skip those
 // blocks and only rows < NT*R/16 are written.
-// LZ: lazy ranges (NT == 16, p < 2^30; modarith.cuh): outputs in [0, 2p).
-template <int KR, int KC, int NT, bool LZ = false>
+// AR: arithmetic mode (modarith.cuh).
+template <int KR, int KC, int NT, int AR = 0>
 __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_fwd_kernel(const FourParams P) {
     using C = ColCfg<KR>;
     constexpr long long Ccols = 1ll << KC;
@@ -41,13 +41,13 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_fwd
     for (int s = 0; s < 16; ++s) {
         const long long idx = (long long)(t + C::G * s) * Ccols + col;
         u32 x = idx < z ? __ldcs(src + idx) : 0u;
-        if (P.reduce) x = mul_t<LZ>(x, 1u, P.red_wp, p);
+        if (P.reduce) x = mul_t<AR>(x, 1u, P.red_wp, p);
         v[s] = x;
     }
     const int zrows = (int)((z + Ccols - 1) / Ccols);
-    fwd_top<KR, NT, LZ>(v, zrows, t, P.cs, W);
+    fwd_top<KR, NT, AR>(v, zrows, t, P.cs, W);
     LayCol<C::TC> lay{c};
-    fwd_lower_chain1<KR, 0, LayCol<C::TC>, NT, LZ>(tile, v, t, P.cs, W, lay);
+    fwd_lower_chain1<KR, 0, LayCol<C::TC>, NT, AR>(tile, v, t, P.cs, W, lay);
     constexpr int SB = last_sb<KR>();
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_fwd
 // Inverse: R-point inverse DIT up each column; truncated (NT < 16): rows
 // >= NT*R/16 hold the column time values, which are zero for a product of
 // length <= NT*L/16, then the van der Hoeven top pass (ItftTop).
-template <int KR, int KC, int NT, bool LZ = false>
+template <int KR, int KC, int NT, int AR = 0>
 __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_inv_kernel(const FourParams P) {
     using C = ColCfg<KR>;
     constexpr long long Ccols = 1ll << KC;
@@ -90,12 +90,12 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_inv
         v[s] = (NT >= 16 || (row >> (KR - 4)) < NT) ? src[(long long)row * Ccols + col] : 0u;
     }
     LayCol<C::TC> lay{c};
-    inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, NT, LZ>(tile, v, t, P.cs, W, lay);
-    ItftTop<KR, 16, NT, 0, LZ>::run(v, t, P.cs, W);
+    inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, NT, AR>(tile, v, t, P.cs, W, lay);
+    inv_top<KR, NT, AR>(v, t, P.cs, W);
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
         const long long idx = (long long)(t + C::G * s) * Ccols + col;
-        if (idx < P.n) __stcs(dst + idx, canon_t<LZ>(v[s], P.cs.p));
+        if (idx < P.n) __stcs(dst + idx, canon_t<(NT < 16 ? 0 : AR)>(v[s], P.cs.p));
     }
 }
 
@@ -104,7 +104,7 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_inv
 // 3-D tensor-map bulk loads into one of two shared buffers while the
 // previous tile is being transformed, so DRAM latency is off the critical
 // path and the 16 strided scalar loads per thread disappear.
-template <int KR, int KC, int NT, bool LZ = false>
+template <int KR, int KC, int NT, int AR = 0>
 __global__ void __launch_bounds__(1024, 1)
 col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
                    const __grid_constant__ CUtensorMap tb, int ntiles) {
@@ -157,16 +157,16 @@ col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
 #pragma unroll
         for (int s = 0; s < 16; ++s) {  // plain row-major tile: conflict-free for this layout
             u32 x = buf[(t + C::G * s) * C::TC + c];
-            if (P.reduce) x = mul_t<LZ>(x, 1u, P.red_wp, p);
+            if (P.reduce) x = mul_t<AR>(x, 1u, P.red_wp, p);
             v[s] = x;
         }
         __syncthreads();  // tile consumed; the other buffer is free since last iteration
         if (threadIdx.x == 0 && tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, k ^ 1);
         const long long z = op ? P.z2 : P.z1;
         const int zrows = (int)((z + Ccols - 1) / Ccols);
-        fwd_top<KR, NT, LZ>(v, zrows, t, P.cs, W);
+        fwd_top<KR, NT, AR>(v, zrows, t, P.cs, W);
         LayCol<C::TC> lay{c};
-        fwd_lower_chain1<KR, 0, LayCol<C::TC>, NT, LZ>(buf, v, t, P.cs, W, lay);
+        fwd_lower_chain1<KR, 0, LayCol<C::TC>, NT, AR>(buf, v, t, P.cs, W, lay);
         u32 *dst = (op ? P.Bh : P.Ah) + (long long)pc * (Ccols << KR);
         const long long col = (long long)ct * C::TC + c;
         constexpr int SB = last_sb<KR>();
@@ -194,7 +194,7 @@ struct ColInvAsync {
     }
 };
 
-template <int KR, int KC, int NT, bool LZ>
+template <int KR, int KC, int NT, int AR>
 __global__ void __launch_bounds__(1024, 1) col_inv_async_kernel(const FourParams P, int ntiles) {
     using C = ColCfg<KR>;
     using A = ColInvAsync<KR>;
@@ -244,32 +244,32 @@ __global__ void __launch_bounds__(1024, 1) col_inv_async_kernel(const FourParams
         __syncthreads();  // tile consumed; the other buffer is free
         if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, k ^ 1);
         LayCol<C::TC> lay{c};
-        inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, NT, LZ>(buf, v, t, P.cs, W, lay);
-        ItftTop<KR, 16, NT, 0, LZ>::run(v, t, P.cs, W);
+        inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, NT, AR>(buf, v, t, P.cs, W, lay);
+        inv_top<KR, NT, AR>(v, t, P.cs, W);
         u32 *dst = P.c + (P.prod0 + pc) * P.ldc;
         const long long col = (long long)ct * C::TC + c;
 #pragma unroll
         for (int s = 0; s < 16; ++s) {
             const long long idx = (long long)(t + C::G * s) * Ccols + col;
-            if (idx < P.n) __stcs(dst + idx, canon_t<LZ>(v[s], P.cs.p));
+            if (idx < P.n) __stcs(dst + idx, canon_t<(NT < 16 ? 0 : AR)>(v[s], P.cs.p));
         }
         k ^= 1;
     }
 }
 
-template <int KR, int KC, int NT, bool LZ>
+template <int KR, int KC, int NT, int AR>
 static cudaError_t launch_inv_async(const FourParams &P, cudaStream_t st) {
     using C = ColCfg<KR>;
     static bool ready = false;
     if (!ready) {
-        cudaError_t e = prep_kernel(col_inv_async_kernel<KR, KC, NT, LZ>, ColInvAsync<KR>::SMEM,
+        cudaError_t e = prep_kernel(col_inv_async_kernel<KR, KC, NT, AR>, ColInvAsync<KR>::SMEM,
                                     C::THREADS, nullptr);
         if (e != cudaSuccess) return e;
         ready = true;
     }
     const int ntiles = (int)((1ll << KC) / C::TC) * P.chunk;
     const int grid = std::min(ntiles, sm_count());
-    col_inv_async_kernel<KR, KC, NT, LZ>
+    col_inv_async_kernel<KR, KC, NT, AR>
         <<<grid, C::THREADS, ColInvAsync<KR>::SMEM, st>>>(P, ntiles);
     return cudaGetLastError();
 }
@@ -281,28 +281,28 @@ static bool col_inv_async_on() {
     return on;
 }
 
-template <int KR, int KC, int NT, bool LZ>
+template <int KR, int KC, int NT, int AR>
 static cudaError_t launch_fwd_tma(const FourParams &P, const ColTma &M, cudaStream_t st) {
     using C = ColCfg<KR>;
     constexpr int SMEM = 2 * C::R * 8 + 2 * C::TILE * 4 + 64;
     static bool ready = false;
     if (!ready) {
-        cudaError_t e = prep_kernel(col_fwd_tma_kernel<KR, KC, NT, LZ>, SMEM, C::THREADS, nullptr);
+        cudaError_t e = prep_kernel(col_fwd_tma_kernel<KR, KC, NT, AR>, SMEM, C::THREADS, nullptr);
         if (e != cudaSuccess) return e;
         ready = true;
     }
     const int ntiles = (int)((1ll << KC) / C::TC) * 2 * P.chunk;
     const int grid = std::min(ntiles, sm_count());
-    col_fwd_tma_kernel<KR, KC, NT, LZ><<<grid, C::THREADS, SMEM, st>>>(P, M.ma, M.mb, ntiles);
+    col_fwd_tma_kernel<KR, KC, NT, AR><<<grid, C::THREADS, SMEM, st>>>(P, M.ma, M.mb, ntiles);
     return cudaGetLastError();
 }
 
-template <int KR, int KC, int NT, bool LZ = false>
+template <int KR, int KC, int NT, int AR = 0>
 static cudaError_t launch_one(const FourParams &P, bool fwd, cudaStream_t st,
                               const ColTma *tma) {
     if constexpr (KR >= 6 && ColCfg<KR>::TILE == 16384) {
-        if (fwd && tma && tma->ok) return launch_fwd_tma<KR, KC, NT, LZ>(P, *tma, st);
-        if (!fwd && col_inv_async_on()) return launch_inv_async<KR, KC, NT, LZ>(P, st);
+        if (fwd && tma && tma->ok) return launch_fwd_tma<KR, KC, NT, AR>(P, *tma, st);
+        if (!fwd && col_inv_async_on()) return launch_inv_async<KR, KC, NT, AR>(P, st);
     }
     using C = ColCfg<KR>;
     static bool ready_f = false, ready_i = false;  // benign races: idempotent
@@ -310,19 +310,19 @@ static cudaError_t launch_one(const FourParams &P, bool fwd, cudaStream_t st,
     if (fwd) {
         if (!ready_f) {
             cudaError_t e =
-                prep_kernel(col_fwd_kernel<KR, KC, NT, LZ>, C::SMEM, C::THREADS, nullptr);
+                prep_kernel(col_fwd_kernel<KR, KC, NT, AR>, C::SMEM, C::THREADS, nullptr);
             if (e != cudaSuccess) return e;
             ready_f = true;
         }
-        col_fwd_kernel<KR, KC, NT, LZ><<<grid, C::THREADS, C::SMEM, st>>>(P);
+        col_fwd_kernel<KR, KC, NT, AR><<<grid, C::THREADS, C::SMEM, st>>>(P);
     } else {
         if (!ready_i) {
             cudaError_t e =
-                prep_kernel(col_inv_kernel<KR, KC, NT, LZ>, C::SMEM, C::THREADS, nullptr);
+                prep_kernel(col_inv_kernel<KR, KC, NT, AR>, C::SMEM, C::THREADS, nullptr);
             if (e != cudaSuccess) return e;
             ready_i = true;
         }
-        col_inv_kernel<KR, KC, NT, LZ><<<grid, C::THREADS, C::SMEM, st>>>(P);
+        col_inv_kernel<KR, KC, NT, AR><<<grid, C::THREADS, C::SMEM, st>>>(P);
     }
     return cudaGetLastError();
 }
@@ -331,16 +331,16 @@ template <int KR, int KC>
 static cudaError_t launch_nt(const FourParams &P, int NT, bool fwd, cudaStream_t st,
                              const ColTma *tma) {
     switch (NT) {
-        case 9: return launch_one<KR, KC, 9>(P, fwd, st, tma);
-        case 10: return launch_one<KR, KC, 10>(P, fwd, st, tma);
-        case 11: return launch_one<KR, KC, 11>(P, fwd, st, tma);
-        case 12: return launch_one<KR, KC, 12>(P, fwd, st, tma);
-        case 13: return launch_one<KR, KC, 13>(P, fwd, st, tma);
-        case 14: return launch_one<KR, KC, 14>(P, fwd, st, tma);
-        case 15: return launch_one<KR, KC, 15>(P, fwd, st, tma);
+        case 9: return launch_one<KR, KC, 9, 2>(P, fwd, st, tma);
+        case 10: return launch_one<KR, KC, 10, 2>(P, fwd, st, tma);
+        case 11: return launch_one<KR, KC, 11, 2>(P, fwd, st, tma);
+        case 12: return launch_one<KR, KC, 12, 2>(P, fwd, st, tma);
+        case 13: return launch_one<KR, KC, 13, 2>(P, fwd, st, tma);
+        case 14: return launch_one<KR, KC, 14, 2>(P, fwd, st, tma);
+        case 15: return launch_one<KR, KC, 15, 2>(P, fwd, st, tma);
         case 16:
-            return P.cs.lazy ? launch_one<KR, KC, 16, true>(P, fwd, st, tma)
-                             : launch_one<KR, KC, 16>(P, fwd, st, tma);
+            return P.cs.ar == 1 ? launch_one<KR, KC, 16, 1>(P, fwd, st, tma)
+                                : launch_one<KR, KC, 16, 2>(P, fwd, st, tma);
         default: return cudaErrorInvalidValue;
     }
 }

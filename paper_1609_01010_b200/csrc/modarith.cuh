@@ -93,32 +93,56 @@ __device__ __forceinline__ void bfly_dit(u32 &a, u32 &b, u32 w, u32 wp, u32 p) {
 }
 
 // ---------------------------------------------------------------- lazy ranges
-// For p < 2^30 (p1, p2; 4p < 2^32) the transforms keep Harvey's lazy ranges:
-// forward DIF values in [0, 2p), inverse DIT values in [0, 4p).  A DIF
-// butterfly then costs 6 instructions instead of 7 and a DIT butterfly 6
-// instead of 8 (profiles/r01/ubench_pipes.txt).  The Montgomery pointwise
-// product accepts [0, 2p) operands when 4p < 2^32 and returns a canonical
-// residue; kernels canonicalise ([0, 4p) -> [0, p)) before every store of a
-// final result.  LZ = false gives the canonical versions above.
-template <bool LZ>
+// Arithmetic modes of the transform kernels (template parameter AR):
+//   AR = 0  canonical residues everywhere (bfly_dif / bfly_dit above).
+//   AR = 1  Harvey's lazy ranges, p < 2^30 (4p < 2^32): forward DIF values in
+//           [0, 2p), inverse DIT values in [0, 4p).  DIF 6 instructions
+//           instead of 7, DIT 6 instead of 8.  The Montgomery pointwise
+//           product accepts [0, 2p) operands when 4p < 2^32.
+//   AR = 2  any p < 2^31: canonical forward; inverse values in [0, 2p).  A
+//           DIT butterfly reduces only its additive input instead of both
+//           outputs (a multiplicand may be any 32-bit word): 7 instructions
+//           instead of 8.
+// Kernels canonicalise (canon_t) before every store of a final result.
+// Building with -DMC_AR_CANON turns modes 1 and 2 into mode 0 (A/B runs).
+#ifdef MC_AR_CANON
+#define MC_AR(ar) 0
+#else
+#define MC_AR(ar) (ar)
+#endif
+
+// forward-side multiply (DIF twiddles, input reduction, forward twists)
+template <int AR>
 __device__ __forceinline__ u32 mul_t(u32 x, u32 w, u32 wp, u32 p) {
     const u32 r = mul_shoup_lazy(x, w, wp, p);
-    return LZ ? r : min(r, r - p);
+    return MC_AR(AR) == 1 ? r : min(r, r - p);
 }
 
-template <bool LZ>
-__device__ __forceinline__ u32 mul_t(u32 x, Shoup s, u32 p) { return mul_t<LZ>(x, s.w, s.wp, p); }
+template <int AR>
+__device__ __forceinline__ u32 mul_t(u32 x, Shoup s, u32 p) { return mul_t<AR>(x, s.w, s.wp, p); }
 
-// a + b of two forward-range values (LZ: [0,2p) each -> [0,2p))
-template <bool LZ>
+// inverse-side multiply (pointwise scale, inverse twists): lazy in modes 1, 2
+template <int AR>
+__device__ __forceinline__ u32 mul_inv_t(u32 x, u32 w, u32 wp, u32 p) {
+    const u32 r = mul_shoup_lazy(x, w, wp, p);
+    return MC_AR(AR) >= 1 ? r : min(r, r - p);
+}
+
+template <int AR>
+__device__ __forceinline__ u32 mul_inv_t(u32 x, Shoup s, u32 p) {
+    return mul_inv_t<AR>(x, s.w, s.wp, p);
+}
+
+// a + b of two forward-range values
+template <int AR>
 __device__ __forceinline__ u32 add_t(u32 a, u32 b, u32 p) {
-    const u32 s = a + b, q = LZ ? 2 * p : p;
+    const u32 s = a + b, q = MC_AR(AR) == 1 ? 2 * p : p;
     return min(s, s - q);
 }
 
-template <bool LZ>
+template <int AR>
 __device__ __forceinline__ void bfly_dif_t(u32 &a, u32 &b, u32 w, u32 wp, u32 p) {
-    if constexpr (LZ) {
+    if constexpr (MC_AR(AR) == 1) {
         const u32 s = a + b;
         b = mul_shoup_lazy(a - b + 2 * p, w, wp, p);
         a = min(s, s - 2 * p);
@@ -128,33 +152,40 @@ __device__ __forceinline__ void bfly_dif_t(u32 &a, u32 &b, u32 w, u32 wp, u32 p)
 }
 
 // DIF butterfly with w = 1
-template <bool LZ>
+template <int AR>
 __device__ __forceinline__ void bfly_dif1_t(u32 &a, u32 &b, u32 p) {
-    const u32 q = LZ ? 2 * p : p;
+    const u32 q = MC_AR(AR) == 1 ? 2 * p : p;
     const u32 s = a + b, d = a - b + q;
     a = min(s, s - q);
     b = min(d, d - q);
 }
 
-template <bool LZ>
+template <int AR>
 __device__ __forceinline__ void bfly_dit_t(u32 &a, u32 &b, u32 w, u32 wp, u32 p) {
-    if constexpr (LZ) {
+    if constexpr (MC_AR(AR) == 1) {  // [0, 4p) in and out
         const u32 x = min(a, a - 2 * p);
         const u32 t = mul_shoup_lazy(b, w, wp, p);
         a = x + t;
         b = x - t + 2 * p;
+    } else if constexpr (MC_AR(AR) == 2) {  // [0, 2p) in and out
+        const u32 x = min(a, a - p);
+        const u32 r = mul_shoup_lazy(b, w, wp, p);
+        const u32 t = min(r, r - p);
+        a = x + t;
+        b = x - t + p;
     } else {
         bfly_dit(a, b, w, wp, p);
     }
 }
 
 // DIT butterfly with w = 1
-template <bool LZ>
+template <int AR>
 __device__ __forceinline__ void bfly_dit1_t(u32 &a, u32 &b, u32 p) {
-    if constexpr (LZ) {
-        const u32 x = min(a, a - 2 * p), y = min(b, b - 2 * p);
+    if constexpr (MC_AR(AR) >= 1) {
+        const u32 q = MC_AR(AR) == 1 ? 2 * p : p;
+        const u32 x = min(a, a - q), y = min(b, b - q);
         a = x + y;
-        b = x - y + 2 * p;
+        b = x - y + q;
     } else {
         const u32 s = a + b, d = a - b + p;
         a = min(s, s - p);
@@ -162,15 +193,12 @@ __device__ __forceinline__ void bfly_dit1_t(u32 &a, u32 &b, u32 p) {
     }
 }
 
-// inverse-range value -> canonical residue (identity when !LZ)
-template <bool LZ>
+// inverse-range value -> canonical residue
+template <int AR>
 __device__ __forceinline__ u32 canon_t(u32 x, u32 p) {
-    if constexpr (LZ) {
-        x = min(x, x - 2 * p);
-        return min(x, x - p);
-    } else {
-        return x;
-    }
+    if constexpr (MC_AR(AR) == 1) x = min(x, x - 2 * p);
+    if constexpr (MC_AR(AR) >= 1) x = min(x, x - p);
+    return x;
 }
 
 }  // namespace mc
