@@ -150,17 +150,20 @@ class ClockSampler:
 
 def cpu_oracle_rate(cfg, threads: int, target_s: float = 10.0, max_products=None):
     """Time the C oracle port of the reference path (products/s) on a
-    bounded sample of the workload.  Returns (products/s, sample description)."""
+    bounded sample of the workload.  Returns (products/s, sample description,
+    threads actually used)."""
     from oracle import oracle
 
     p, z1, z2 = cfg["p"], cfg["z1"], cfg["z2"]
     if cfg["engine"] == "three_primes":
         a = oracle.gen_u32(cfg["seed"], 0, 0, 1, z1, 1 << 30)[0]
         b = oracle.gen_u32(cfg["seed"], 1, 0, 1, z2, 1 << 30)[0]
+        used = min(3, threads)  # one thread per prime (SURVEY 8d), serial Garner
         t0 = time.perf_counter()
-        oracle.mul_three_primes(a, b)
+        oracle.mul_three_primes(a, b, threads=used)
         dt = time.perf_counter() - t0
-        return 1.0 / dt, "1 three-primes product (3 x fft_pad 2^21 + Garner), 1 thread"
+        return 1.0 / dt, (f"1 three-primes product (3 x fft_pad 2^21 + Garner), "
+                          f"{used} threads (one per prime)"), used
     engine = oracle.ENGINE_TFT if cfg["engine"] == "tft" else oracle.ENGINE_FFT_PAD
     B = cfg["batch"]
     # calibrate on a small slice
@@ -178,7 +181,7 @@ def cpu_oracle_rate(cfg, threads: int, target_s: float = 10.0, max_products=None
     t0 = time.perf_counter()
     oracle.conv_batch(a, b, p, engine, threads=threads)
     dt = time.perf_counter() - t0
-    return nsamp / dt, f"{nsamp} of {B} products (rows 0..{nsamp - 1}), {threads} threads"
+    return nsamp / dt, f"{nsamp} of {B} products (rows 0..{nsamp - 1}), {threads} threads", threads
 
 
 def host_threads() -> int:
@@ -203,7 +206,7 @@ def run_reference(args, cfg):
     rates = []
     sample = None
     for i in range(args.warmup + args.steps):
-        r, sample = cpu_oracle_rate(cfg, threads, target_s=args.ref_step_seconds)
+        r, sample, used = cpu_oracle_rate(cfg, threads, target_s=args.ref_step_seconds)
         if i >= args.warmup:
             rates.append(r)
     v = statistics.median(rates)
@@ -215,7 +218,7 @@ def run_reference(args, cfg):
         "config": {"workload": cfg["name"], "batch": cfg["batch"], "z1": cfg["z1"],
                    "z2": cfg["z2"], "n": n, "p": cfg["p"], "engine": cfg["engine"]},
         "gcoeff_per_s": v * n / 1e9,
-        "cpu_baseline": {"value": v, "unit": "products/s", "cores": threads, "kind": "port",
+        "cpu_baseline": {"value": v, "unit": "products/s", "cores": used, "kind": "port",
                          "sample": sample + " per step; C restatement of the reference "
                                             "(oracle/modconv_oracle.c)"},
         "e2e": {"value": v, "unit": "products/s", "h2d_bytes_per_step": 0,
@@ -418,7 +421,7 @@ def run_mine(args, cfg):
         bf, pw = 3 * full_count(L), L
     else:
         bf, pw = 3 * 3 * full_count(L), 3 * L
-    cpu_rate, sample = cpu_oracle_rate(cfg, host_threads(), target_s=args.ref_seconds)
+    cpu_rate, sample, cpu_cores = cpu_oracle_rate(cfg, host_threads(), target_s=args.ref_seconds)
     line = {
         "metric": "modular poly-mults/sec", "value": value, "unit": "products/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
@@ -439,7 +442,7 @@ def run_mine(args, cfg):
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk,
-        "cpu_baseline": {"value": cpu_rate, "unit": "products/s", "cores": host_threads(),
+        "cpu_baseline": {"value": cpu_rate, "unit": "products/s", "cores": cpu_cores,
                          "kind": "port", "sample": sample},
     }
     print(json.dumps(line), flush=True)

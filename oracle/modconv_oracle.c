@@ -297,7 +297,13 @@ int64_t orc_moddft(u32 p, int log2L, const u32 *x, u32 *y, int inverse) {
     orc_table t;
     if (table_init(&t, p, log2L)) return -1;
     int64_t L = t.size;
-    u64 *in = (u64 *)malloc(8 * L), *out = (u64 *)malloc(8 * L);
+    u64 *in = (u64 *)calloc((size_t)L, 8), *out = (u64 *)malloc(8 * L);
+    if (!in || !out) {
+        free(in);
+        free(out);
+        table_free(&t);
+        return -2;
+    }
     for (int64_t i = 0; i < L; ++i) in[i] = x[i];
     moddft_t(&t, in, out, inverse);
     for (int64_t i = 0; i < L; ++i) y[i] = (u32)out[i];
@@ -476,28 +482,59 @@ void orc_crt3(u32 p1, u32 p2, u32 p3, const u32 *r1, const u32 *r2, const u32 *r
 }
 
 /* Full three-primes multiply over Z (oracle): integer inputs < 2^32 reduced
- * mod each prime (poly.py:46-49 from_ints), fft_pad per prime, then Garner. */
+ * mod each prime (poly.py:46-49 from_ints), fft_pad per prime, then Garner.
+ * threads >= 3 runs the three primes concurrently (one process
+ * per prime); the Garner step is serial. */
+typedef struct {
+    u32 p;
+    const u32 *a, *b;
+    int64_t z1, z2, n;
+    u32 *res;
+    int rc;
+} prime_job;
+
+static void *prime_worker(void *arg) {
+    prime_job *j = (prime_job *)arg;
+    u32 *ra = (u32 *)malloc(4 * j->z1), *rb = (u32 *)malloc(4 * j->z2);
+    if (!ra || !rb) {
+        free(ra);
+        free(rb);
+        j->rc = 1;
+        return NULL;
+    }
+    for (int64_t i = 0; i < j->z1; ++i) ra[i] = j->a[i] % j->p;
+    for (int64_t i = 0; i < j->z2; ++i) rb[i] = j->b[i] % j->p;
+    j->rc = orc_conv_batch(j->p, 0, ra, j->z1, j->z1, rb, j->z2, j->z2, j->res, j->n, 1, 1, NULL);
+    free(ra);
+    free(rb);
+    return NULL;
+}
+
 int orc_mul_three_primes(const u32 *a, int64_t z1, const u32 *b, int64_t z2,
                          u32 *limbs, int threads) {
     static const u32 P[3] = {469762049u, 998244353u, 2013265921u};
     int64_t n = z1 + z2 - 1;
-    u32 *ra = (u32 *)malloc(4 * z1), *rb = (u32 *)malloc(4 * z2);
     u32 *res = (u32 *)malloc(4 * 3 * n);
-    (void)threads;
+    if (!res) return 1;
+    prime_job jobs[3];
+    pthread_t th[3];
+    int started[3] = {0, 0, 0};
     for (int k = 0; k < 3; ++k) {
-        for (int64_t i = 0; i < z1; ++i) ra[i] = a[i] % P[k];
-        for (int64_t i = 0; i < z2; ++i) rb[i] = b[i] % P[k];
-        int rc = orc_conv_batch(P[k], 0, ra, z1, z1, rb, z2, z2, res + k * n, n, 1, 1, NULL);
-        if (rc) {
-            free(ra); free(rb); free(res);
-            return rc;
-        }
+        prime_job j = {P[k], a, b, z1, z2, n, res + k * n, 0};
+        jobs[k] = j;
+        if (threads >= 3 && pthread_create(&th[k], NULL, prime_worker, &jobs[k]) == 0)
+            started[k] = 1;
+        else
+            prime_worker(&jobs[k]);
     }
-    orc_crt3(P[0], P[1], P[2], res, res + n, res + 2 * n, n, limbs);
-    free(ra);
-    free(rb);
+    int rc = 0;
+    for (int k = 0; k < 3; ++k) {
+        if (started[k]) pthread_join(th[k], NULL);
+        if (jobs[k].rc) rc = jobs[k].rc;
+    }
+    if (!rc) orc_crt3(P[0], P[1], P[2], res, res + n, res + 2 * n, n, limbs);
     free(res);
-    return 0;
+    return rc;
 }
 
 /* Op counts of the reference recursions without doing arithmetic

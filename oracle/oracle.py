@@ -181,11 +181,11 @@ def crt3(r1, r2, r3, primes=(469762049, 998244353, 2013265921)) -> np.ndarray:
     return limbs
 
 
-def mul_three_primes(a, b) -> np.ndarray:
+def mul_three_primes(a, b, threads: int = 1) -> np.ndarray:
     a, b = _u32(a), _u32(b)
     n = a.size + b.size - 1
     limbs = np.empty((3, n), dtype=np.uint32)
-    _check(lib().orc_mul_three_primes(_ptr(a), a.size, _ptr(b), b.size, _ptr(limbs), 1))
+    _check(lib().orc_mul_three_primes(_ptr(a), a.size, _ptr(b), b.size, _ptr(limbs), threads))
     return limbs
 
 

@@ -6,5 +6,5 @@ python bench.py --impl reference > gpurun_out/final_ref.json 2>&1; head -c 400 g
 python scripts/ubench.py > gpurun_out/ubench.json 2>&1
 python bench.py --steps 2 --warmup 3 --ref-seconds 0.1 > gpurun_out/fplain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file gpurun_out/final_launches_cfg2.csv python bench.py --steps 2 --warmup 3 --ref-seconds 0.1 > gpurun_out/fncu1.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:conv_small -s 2 -c 1 -o gpurun_out/prof_cfg2_v8 python bench.py --steps 2 --warmup 3 --ref-seconds 0.1 > gpurun_out/fncu2.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:conv_small -s 2 -c 1 -o gpurun_out/prof_cfg2_final python bench.py --steps 2 --warmup 3 --ref-seconds 0.1 > gpurun_out/fncu2.log 2>&1
 echo "ncu rc=$?"
