@@ -1,6 +1,7 @@
 // C ABI entry points (include/modconv_b200.h): argument checking, table
 // lookup, kernel selection.  No torch types cross this boundary.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -101,7 +102,8 @@ static cudaError_t launch_small(int K, const ConvSmallParams &P, int nt, cudaStr
 static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, const u32 *b,
                                long long ldb, int z2, u32 *c, long long ldc, long long batch,
                                u32 p, cudaStream_t st, int circ_log2L = -1,
-                               bool reduce = false) {
+                               bool reduce = false, bool allow_tma = true,
+                               bool host_out = false) {
     if (z1 < 1 || z2 < 1) return fail(MC_EINVAL, "inputs must be nonempty");
     if (batch < 0) return fail(MC_EINVAL, "negative batch");
     if (lda < z1 || ldb < z2) return fail(MC_EINVAL, "leading dimension smaller than row length");
@@ -134,7 +136,7 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
             const int za16 = z1 & ~3, zb16 = z2 & ~3;
             const long long smem = 2ll * (1 << K) * 8 + 2ll * (1 << K) * 4 + 16 +
                                    4ll * (za16 + zb16);  // upper bound (tables in smem)
-            if (one_per_cta && aligned && smem <= 227 * 1024 && batch > 0) {
+            if (allow_tma && one_per_cta && aligned && smem <= 227 * 1024 && batch > 0) {
                 P.tma = 1;
                 P.za16 = za16;
                 P.zb16 = zb16;
@@ -148,6 +150,10 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
         if (batch > 0x7fffffffll * SmallCfg<4>::PPC)
             return fail(MC_EINVAL, "batch too large for one launch");
         P.ar = (nt == 16 && lazy_ok(p)) ? 1 : 2;
+        {  // bulk-copy epilogue: host output (zero copy), or forced for A/B runs
+            static const bool force = [] { const char *e = getenv("MC_BULK_OUT"); return e && *e; }();
+            P.bulk_out = ((host_out || force) && (1 << K) / 16 >= 128) ? 1 : 0;
+        }
         cudaError_t e = launch_small(K, P, nt, st);
         note_launches(1);
         if (e != cudaSuccess) return cuda_fail(e, "conv_small launch");
@@ -246,6 +252,30 @@ struct PipeState {
 
 static std::mutex g_pipe_mu;
 
+// Shapes zero copy suits: the fused single-pass kernel (every operand word
+// read once, every product word written once) with one product per CTA
+// (bulk-store epilogue), or any fused size when the whole call moves under
+// 1 MiB (latency bound: no pipeline start-up).
+static bool zero_copy_shape(int64_t n, int64_t batch) {
+    int K = 0;
+    while ((1ll << K) < n) ++K;
+    if (K < 4 || K > kSmallMaxK) return false;
+    return K >= 11 || 8 * n * batch < (1ll << 20);
+}
+
+// Host memory the device can address directly (page-locked, mapped into the
+// unified address space at the same pointer).  MC_NO_ZERO_COPY disables.
+static bool zero_copy_ok(const void *ptr) {
+    static const bool off = [] { const char *e = getenv("MC_NO_ZERO_COPY"); return e && *e; }();
+    if (off) return false;
+    cudaPointerAttributes at;
+    if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return at.type == cudaMemoryTypeHost && at.devicePointer == ptr;
+}
+
 mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t z1,
                              const uint32_t *b, int64_t ldb, int32_t z2, uint32_t *c,
                              int64_t ldc, int64_t batch, uint32_t p, int64_t chunk_rows,
@@ -265,6 +295,16 @@ mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t
         if (st != MC_OK) return st;
     }
     cudaStream_t user = (cudaStream_t)stream;
+    if (zero_copy_shape(n, batch) && zero_copy_ok(a) && zero_copy_ok(b) && zero_copy_ok(c)) {
+        // Zero copy: page-locked host rows are device-addressable (UVA), so the
+        // fused kernel reads the operands (bulk-copy prefetch of the next
+        // product's rows) and writes the products (bulk stores from shared
+        // memory) over PCIe itself, reads and writes of different CTAs
+        // overlapping; no copy-engine chunks (measured ~40 us of overhead per
+        // chunk in the copy pipeline).
+        return conv_dispatch(engine, a, lda, z1, b, ldb, z2, c, ldc, batch, p, user, -1, false,
+                             true, true);
+    }
     const int dev = current_device();
     if (S.dev != dev) {
         std::lock_guard<std::mutex> lock(g_pipe_mu);

@@ -61,6 +61,8 @@ struct ConvSmallParams {
     uint2 c16f[16];    // tf[1..15] / ti[1..15]: the thread-invariant twiddles of the
     uint2 c16i[16];    // lowest pass (h <= 8), read from the constant bank
     int ar;            // arithmetic mode of the launch (modarith.cuh): 1 or 2
+    int bulk_out;      // write product rows by bulk copies from shared memory (PPC == 1;
+                       // zero-copy host output)
 };
 
 // 32-bank conflict-free swizzle for the three access patterns used here:
@@ -536,6 +538,9 @@ conv_small_kernel(const ConvSmallParams P) {
 
         fwd_top<K, NT, AR>(va, P.z1, t, P, W);
         fwd_top<K, NT, AR>(vb, P.z2, t, P, W);
+        // the previous product's bulk store has read its staging before the
+        // first exchange (after the barrier inside the chain) reuses bufA
+        if (C::PPC == 1 && P.bulk_out && threadIdx.x == 0) bulk_wait_read_all();
         fwd_lower_chain<K, NT, 0, AR>(bufA, bufB, va, vb, t, P, W);
 
         // pointwise product in the last pass's layout, L^-1 folded in
@@ -567,7 +572,29 @@ conv_small_kernel(const ConvSmallParams P) {
         inv_lower_chain<K, NT, Plan<K>::NP - 1, AR>(bufA, va, t, P, W);
         inv_top<K, NT, AR>(va, t, P, W);
 
-        if (valid) {
+        if (C::PPC == 1 && P.bulk_out) {
+            // Stage the row in bufA (idle after the last inverse exchange; up to
+            // 3 words spill into bufB, idle too) at the destination's offset mod
+            // 16 bytes, then one bulk store of the aligned interior; the <= 3
+            // head and tail words go out as plain stores.
+            u32 *gc = P.c + row * P.ldc;
+            const int mis = (int)(((uintptr_t)gc >> 2) & 3);
+            u32 *stg = bufA + mis;
+            __syncthreads();  // every thread is done reading bufA
+#pragma unroll
+            for (int s = 0; s < 16; ++s)
+                stg[(s << (K - 4)) | t] = canon_t<(NT < 16 ? 0 : AR)>(va[s], P.p);
+            fence_proxy_async_smem();
+            __syncthreads();
+            const int head = min((4 - mis) & 3, P.n);
+            const int nb = ((P.n - head) >> 2) << 2;  // words in the bulk part
+            if (threadIdx.x == 0 && nb > 0) {
+                bulk_s2g(gc + head, stg + head, 4u * nb);
+                bulk_commit();
+            }
+            if (t < head) gc[t] = stg[t];
+            if (head + nb + t < P.n) gc[head + nb + t] = stg[head + nb + t];
+        } else if (valid) {
             u32 *gc = P.c + row * P.ldc;
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
@@ -576,6 +603,7 @@ conv_small_kernel(const ConvSmallParams P) {
             }
         }
     }
+    if (C::PPC == 1 && P.bulk_out && threadIdx.x == 0) bulk_wait_all();
 }
 
 }  // namespace mc

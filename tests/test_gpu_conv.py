@@ -153,6 +153,39 @@ def test_strided_rows_and_host_buffers(orc):
     assert np.array_equal(got.numpy().view(np.uint32), want)
 
 
+@pytest.mark.parametrize("engine", ["fft_pad", "tft"])
+def test_host_buffers_zero_copy_and_pipeline(orc, engine):
+    """Host tensors: page-locked rows (zero copy: the kernel reads and writes
+    host memory directly, strided rows included) and pageable rows (chunked
+    copy pipeline) give the same bit-exact products."""
+    p = P2
+    B, z1, z2 = 700, 1500, 2100
+    a = orc.gen_u32(22, 0, 0, B, z1, p)
+    b = orc.gen_u32(22, 1, 0, B, z2, p)
+    a[3, :] = p - 1
+    b[3, :] = p - 1
+    want, _, _ = orc.conv_batch(a, b, p, 1 if engine == "tft" else 0, threads=8)
+    at = torch.from_numpy(a.view(np.int32))
+    bt = torch.from_numpy(b.view(np.int32))
+    # pinned, contiguous; output allocated by the call
+    got = mc.conv_batch(at.pin_memory(), bt.pin_memory(), p, engine=engine)
+    assert got.device.type == "cpu"
+    assert np.array_equal(got.numpy().view(np.uint32), want)
+    # pinned, strided rows in and out
+    ap = torch.zeros((B, z1 + 37), dtype=torch.int32).pin_memory()
+    bp = torch.zeros((B, z2 + 5), dtype=torch.int32).pin_memory()
+    ap[:, :z1] = at
+    bp[:, :z2] = bt
+    cp = torch.full((B, z1 + z2 + 11), -1, dtype=torch.int32).pin_memory()
+    out = cp[:, : z1 + z2 - 1]
+    mc.conv_batch(ap[:, :z1], bp[:, :z2], p, engine=engine, out=out)
+    assert np.array_equal(out.numpy().view(np.uint32), want)
+    assert (cp[:, z1 + z2 - 1:] == -1).all()  # nothing written past n
+    # pageable: the chunked copy pipeline
+    got = mc.conv_batch(at.clone(), bt.clone(), p, engine=engine)
+    assert np.array_equal(got.numpy().view(np.uint32), want)
+
+
 def test_list_api_poly_mul(golden_small):
     for c in golden_small["poly_mul"]:
         fp = mc.FourierPrime.from_modulus(c["p"])
