@@ -164,14 +164,18 @@ mc_status mc_conv_host(int engine, const uint32_t *a, int64_t lda, int32_t z1,
                        const uint32_t *b, int64_t ldb, int32_t z2, uint32_t *c,
                        int64_t ldc, int64_t batch, uint32_t p);
 
-/* Host-buffer batched call, asynchronous and pipelined: the batch is cut
- * into chunks of `chunk_rows` products (0 = automatic); for each chunk the
- * H2D copy of its operand rows, the convolution kernel and the D2H copy of
- * its products run on three internal streams, so copies in both directions
- * overlap each other and the kernels.  The call is ordered after prior work
- * on `stream` and `stream` waits for the last D2H before later work.  Host
- * buffers should be pinned (cudaHostAlloc) for the copies to overlap.  The
- * caller must not touch c before synchronizing `stream`. */
+/* Host-buffer batched call, asynchronous.  When a, b and c are page-locked
+ * host memory mapped into the unified address space (cudaHostAlloc, torch
+ * pin_memory) and the product fits the fused kernel (L <= 8192), the kernel
+ * reads the operand rows and writes the products over PCIe itself (zero
+ * copy: bulk-copy prefetch in, bulk stores out; MC_NO_ZERO_COPY disables).
+ * Otherwise the batch is cut into chunks of `chunk_rows` products
+ * (0 = automatic); for each chunk the H2D copy of its operand rows, the
+ * convolution kernel and the D2H copy of its products run on three internal
+ * streams, so copies in both directions overlap each other and the kernels.
+ * The call is ordered after prior work on `stream` and `stream` waits for the
+ * last write of c before later work.  The caller must not touch c before
+ * synchronizing `stream`. */
 mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t z1,
                              const uint32_t *b, int64_t ldb, int32_t z2, uint32_t *c,
                              int64_t ldc, int64_t batch, uint32_t p, int64_t chunk_rows,
