@@ -2,6 +2,8 @@
 // lookup, kernel selection.  No torch types cross this boundary.
 #include <algorithm>
 #include <cstdlib>
+
+#include <cuda.h>
 #include <cstring>
 #include <mutex>
 
@@ -98,12 +100,20 @@ static cudaError_t launch_small(int K, const ConvSmallParams &P, int nt, cudaStr
     }
 }
 
+// Inputs that a copy stream is still delivering when the kernel starts: the
+// rows of chunk i (rows products each) are resident once flags[i] == epoch.
+struct StreamIn {
+    const uint32_t *flags;
+    uint32_t epoch;
+    int rows;
+};
+
 // engine 0 = fft_pad, 1 = tft; wrap != 0 => circular convolution of length L
 static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, const u32 *b,
                                long long ldb, int z2, u32 *c, long long ldc, long long batch,
                                u32 p, cudaStream_t st, int circ_log2L = -1,
                                bool reduce = false, bool allow_tma = true,
-                               bool host_out = false) {
+                               bool host_out = false, const StreamIn *sin = nullptr) {
     if (z1 < 1 || z2 < 1) return fail(MC_EINVAL, "inputs must be nonempty");
     if (batch < 0) return fail(MC_EINVAL, "negative batch");
     if (lda < z1 || ldb < z2) return fail(MC_EINVAL, "leading dimension smaller than row length");
@@ -141,6 +151,12 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
                 P.za16 = za16;
                 P.zb16 = zb16;
             }
+        }
+        if (sin) {  // streamed inputs: only the bulk-copy prefetch can wait for them
+            if (!P.tma) return fail(MC_EINVAL, "streamed inputs need the bulk-copy path");
+            P.ready = sin->flags;
+            P.epoch = sin->epoch;
+            P.ready_rows = sin->rows;
         }
         int nt = 16;
         if (engine == 1 && !circ) {
@@ -248,19 +264,54 @@ struct PipeState {
     cudaEvent_t ev_in[NBUF] = {}, ev_cmp[NBUF] = {}, ev_out[NBUF] = {}, ev_start = nullptr;
     void *buf = nullptr;
     size_t bytes = 0;
+    // streamed-input mode: whole-batch operand buffer + per-chunk ready flags
+    static constexpr int MAX_CHUNKS = 1 << 16;
+    void *in_buf = nullptr;
+    size_t in_bytes = 0;
+    uint32_t *flags = nullptr;
+    uint32_t epoch = 0;
+    cudaEvent_t ev_k = nullptr, ev_cp = nullptr;
+    // recorded on the caller's stream at the end of every call: the next call's
+    // internal streams wait on it, so reused buffers are never overwritten
+    // while an earlier call (possibly on another caller stream) still uses them
+    cudaEvent_t ev_done = nullptr;
 };
+
+// cuStreamWriteValue32 through the runtime's driver entry point (no libcuda link)
+typedef CUresult (*PFN_write_value32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_write_value32 write_value32() {
+    static PFN_write_value32 fn = [] {
+        void *f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_write_value32>(f);
+    }();
+    return fn;
+}
 
 static std::mutex g_pipe_mu;
 
-// Shapes zero copy suits: the fused single-pass kernel (every operand word
-// read once, every product word written once) with one product per CTA
-// (bulk-store epilogue), or any fused size when the whole call moves under
-// 1 MiB (latency bound: no pipeline start-up).
-static bool zero_copy_shape(int64_t n, int64_t batch) {
+// Host-memory modes for the fused single-pass kernel (every operand word
+// read once, every product word written once), from measurements on B200
+// (DESIGN.md section 7):
+//   2  zero copy (the kernel reads and writes page-locked host memory):
+//      calls under 8 MiB (latency bound), and one-product-per-CTA sizes
+//      (L >= 2048, bulk-store epilogue) with under 512 MiB of operands;
+//   1  streamed inputs + zero-copy output (stream_in_call): one-product-per-
+//      CTA sizes with >= 512 MiB of operands (large copy-engine chunks);
+//   0  chunked copy pipeline (other sizes).
+static int zero_copy_shape(int64_t n, int64_t z12, int64_t batch) {
     int K = 0;
     while ((1ll << K) < n) ++K;
-    if (K < 4 || K > kSmallMaxK) return false;
-    return K >= 11 || 8 * n * batch < (1ll << 20);
+    if (K < 4 || K > kSmallMaxK) return 0;
+    if (8 * n * batch < (8ll << 20)) return 2;
+    if (K < 11) return 0;
+    const char *e = getenv("MC_STREAM_IN_MIN_MB");  // read per call (tests force the mode)
+    const long long min_mb = e && *e ? atoll(e) : 512;
+    return 4 * z12 * batch < (min_mb << 20) ? 2 : 1;
 }
 
 // Host memory the device can address directly (page-locked, mapped into the
@@ -274,6 +325,91 @@ static bool zero_copy_ok(const void *ptr) {
         return false;
     }
     return at.type == cudaMemoryTypeHost && at.devicePointer == ptr;
+}
+
+// Streamed inputs, page-locked output: the operand rows go H2D in chunks on a
+// copy stream, each chunk followed by a stream-memory write of its ready
+// flag; ONE persistent fused kernel, launched at once, waits per product for
+// its chunk's flag before the bulk-copy prefetch and writes its products
+// straight into host memory with bulk stores.  Copy-engine reads and
+// kernel writes share PCIe (~44 GB/s each way measured), with no per-chunk
+// kernel drain.  Returns 1 (not applicable) to fall back to the pipeline.
+static int stream_in_call(PipeState &S, int engine, const uint32_t *a, int64_t lda, int32_t z1,
+                          const uint32_t *b, int64_t ldb, int32_t z2, uint32_t *c, int64_t ldc,
+                          int64_t batch, uint32_t p, cudaStream_t user, mc_status *out) {
+    static const bool off = [] { const char *e = getenv("MC_NO_STREAM_IN"); return e && *e; }();
+    auto wv = write_value32();
+    if (off || !wv) return 1;
+    const int64_t lda_d = (z1 + 3) & ~3ll, ldb_d = (z2 + 3) & ~3ll;  // 16-byte rows
+    const size_t need = 4ull * batch * (lda_d + ldb_d);
+    if (need > (4ull << 30)) return 1;
+    // 32 uniform chunks: used only for >= 512 MiB of operands, so every copy
+    // is large (a copy-engine call costs ~10-20 us; geometric chunk sizes were
+    // measured worse: the kernel stalls on the last, largest chunk)
+    const int64_t rows = std::max<int64_t>(16, (batch + 31) / 32);
+    const int64_t nch = (batch + rows - 1) / rows;
+    if (nch > PipeState::MAX_CHUNKS || rows > 0x7fffffff) return 1;
+    auto fail_out = [&](mc_status st) { *out = st; return 0; };
+    if (!S.flags) {
+        if (cudaMalloc(&S.flags, 4ull * PipeState::MAX_CHUNKS) != cudaSuccess ||
+            cudaMemset(S.flags, 0, 4ull * PipeState::MAX_CHUNKS) != cudaSuccess ||
+            cudaEventCreateWithFlags(&S.ev_k, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&S.ev_cp, cudaEventDisableTiming) != cudaSuccess)
+            return fail_out(cuda_fail(cudaGetLastError(), "stream-in state"));
+    }
+    if (S.in_bytes < need) {
+        cudaDeviceSynchronize();  // the previous call's kernel may still read in_buf
+        if (S.in_buf) cudaFree(S.in_buf);
+        S.in_buf = nullptr;
+        S.in_bytes = 0;
+        if (cudaMalloc(&S.in_buf, need) != cudaSuccess)
+            return fail_out(cuda_fail(cudaGetLastError(), "stream-in buffer"));
+        S.in_bytes = need;
+    }
+    if (++S.epoch == 0) S.epoch = 1;
+    uint32_t *da = (uint32_t *)S.in_buf, *db = da + batch * lda_d;
+    // both streams start after prior work on the user's stream (this also
+    // orders the copies after the previous call's kernel, which read in_buf)
+    if (cudaEventRecord(S.ev_start, user) != cudaSuccess ||
+        cudaStreamWaitEvent(S.s_in, S.ev_start, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(S.s_cmp, S.ev_start, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(S.s_in, S.ev_done, 0) != cudaSuccess)
+        return fail_out(cuda_fail(cudaGetLastError(), "stream-in ordering"));
+    for (int64_t i = 0; i < nch; ++i) {
+        const int64_t r0 = i * rows, nr = std::min(rows, batch - r0);
+        // one linear DMA per operand chunk when the rows are contiguous on both
+        // sides (pitched copies of short rows run far below PCIe speed)
+        auto copy = [&](uint32_t *dst, int64_t ldd, const uint32_t *src, int64_t lds, int32_t z) {
+            if (lds == z && ldd == z)
+                return cudaMemcpyAsync(dst + r0 * ldd, src + r0 * lds, 4ull * z * nr,
+                                       cudaMemcpyHostToDevice, S.s_in);
+            return cudaMemcpy2DAsync(dst + r0 * ldd, 4 * ldd, src + r0 * lds, 4 * lds, 4 * z, nr,
+                                     cudaMemcpyHostToDevice, S.s_in);
+        };
+        if (copy(da, lda_d, a, lda, z1) != cudaSuccess || copy(db, ldb_d, b, ldb, z2) != cudaSuccess)
+            return fail_out(cuda_fail(cudaGetLastError(), "stream-in copy"));
+        if (wv((CUstream)S.s_in, (CUdeviceptr)(S.flags + i), S.epoch, CU_STREAM_WRITE_VALUE_DEFAULT) !=
+            CUDA_SUCCESS) {
+            // the kernel would wait forever: drain the copies, report
+            cudaStreamSynchronize(S.s_in);
+            return fail_out(fail(MC_ECUDA, "cuStreamWriteValue32 failed"));
+        }
+    }
+    const StreamIn sin{S.flags, S.epoch, (int)rows};
+    mc_status st = conv_dispatch(engine, da, lda_d, z1, db, ldb_d, z2, c, ldc, batch, p, S.s_cmp,
+                                 -1, false, true, true, &sin);
+    if (st != MC_OK) {
+        cudaStreamSynchronize(S.s_in);
+        return fail_out(st);
+    }
+    if (cudaEventRecord(S.ev_k, S.s_cmp) != cudaSuccess ||
+        cudaEventRecord(S.ev_cp, S.s_in) != cudaSuccess ||
+        cudaStreamWaitEvent(user, S.ev_k, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(user, S.ev_cp, 0) != cudaSuccess ||
+        cudaEventRecord(S.ev_done, user) != cudaSuccess)
+        return fail_out(cuda_fail(cudaGetLastError(), "stream-in join"));
+    *out = MC_OK;
+    return 0;
 }
 
 mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t z1,
@@ -295,16 +431,20 @@ mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t
         if (st != MC_OK) return st;
     }
     cudaStream_t user = (cudaStream_t)stream;
-    if (zero_copy_shape(n, batch) && zero_copy_ok(a) && zero_copy_ok(b) && zero_copy_ok(c)) {
+    const int zc = zero_copy_shape(n, (int64_t)z1 + z2, batch);
+    const bool c_mapped = zc && zero_copy_ok(c);
+    if (zc == 2 && c_mapped && zero_copy_ok(a) && zero_copy_ok(b)) {
         // Zero copy: page-locked host rows are device-addressable (UVA), so the
-        // fused kernel reads the operands (bulk-copy prefetch of the next
-        // product's rows) and writes the products (bulk stores from shared
-        // memory) over PCIe itself, reads and writes of different CTAs
-        // overlapping; no copy-engine chunks (measured ~40 us of overhead per
-        // chunk in the copy pipeline).
+        // fused kernel reads the operands (bulk-copy prefetch) and writes the
+        // products (bulk stores from shared memory) over PCIe itself -- no
+        // copy-engine calls (~10-20 us each) and no pipeline start-up.
         return conv_dispatch(engine, a, lda, z1, b, ldb, z2, c, ldc, batch, p, user, -1, false,
                              true, true);
     }
+    // Large calls with a page-locked output: streamed inputs (stream_in_call).
+    // Measured on cfg2 shapes: copy-engine H2D alongside kernel bulk writes to
+    // host reaches ~44 GB/s each way; kernel reads from host alongside any
+    // host writes only ~36 (scripts/zc_probe{2,3,4}.py).
     const int dev = current_device();
     if (S.dev != dev) {
         std::lock_guard<std::mutex> lock(g_pipe_mu);
@@ -317,9 +457,18 @@ mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t
             MC_CUDA_CHECK(cudaEventCreateWithFlags(&S.ev_out[k], cudaEventDisableTiming));
         }
         MC_CUDA_CHECK(cudaEventCreateWithFlags(&S.ev_start, cudaEventDisableTiming));
+        MC_CUDA_CHECK(cudaEventCreateWithFlags(&S.ev_done, cudaEventDisableTiming));
         S.dev = dev;
         S.buf = nullptr;
         S.bytes = 0;
+        S.in_buf = nullptr;
+        S.in_bytes = 0;
+        S.flags = nullptr;
+    }
+    if (zc == 1 && c_mapped) {
+        mc_status st = MC_OK;
+        if (stream_in_call(S, engine, a, lda, z1, b, ldb, z2, c, ldc, batch, p, user, &st) == 0)
+            return st;
     }
     if (chunk_rows <= 0) {  // ~8 chunks, at least 64 rows, at most ~16 MiB of operands
         chunk_rows = std::max<int64_t>(64, (batch + 7) / 8);
@@ -340,6 +489,7 @@ mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t
     }
     MC_CUDA_CHECK(cudaEventRecord(S.ev_start, user));
     MC_CUDA_CHECK(cudaStreamWaitEvent(S.s_in, S.ev_start, 0));
+    MC_CUDA_CHECK(cudaStreamWaitEvent(S.s_in, S.ev_done, 0));
     const int64_t nch = (batch + chunk_rows - 1) / chunk_rows;
     for (int64_t i = 0; i < nch; ++i) {
         const int k = (int)(i % PipeState::NBUF);
@@ -374,9 +524,10 @@ mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t
                                             cudaMemcpyDeviceToHost, S.s_out));
         MC_CUDA_CHECK(cudaEventRecord(S.ev_out[k], S.s_out));
     }
-    // the user's stream continues after the last D2H
+    // the user's stream continues after the last write of c
     const int last = (int)((nch - 1) % PipeState::NBUF);
     MC_CUDA_CHECK(cudaStreamWaitEvent(user, S.ev_out[last], 0));
+    MC_CUDA_CHECK(cudaEventRecord(S.ev_done, user));
     return MC_OK;
 }
 

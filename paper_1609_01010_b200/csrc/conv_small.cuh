@@ -63,6 +63,9 @@ struct ConvSmallParams {
     int ar;            // arithmetic mode of the launch (modarith.cuh): 1 or 2
     int bulk_out;      // write product rows by bulk copies from shared memory (PPC == 1;
                        // zero-copy host output)
+    const uint32_t *ready;  // streamed inputs (PPC == 1 with TMA): rows of chunk i are
+    uint32_t epoch;         // resident once ready[i] == epoch (set by the copy stream)
+    int ready_rows;         // products per chunk
 };
 
 // 32-bank conflict-free swizzle for the three access patterns used here:
@@ -475,6 +478,11 @@ conv_small_kernel(const ConvSmallParams P) {
     u32 *stB = stA + P.za16;
     auto prefetch = [&](long long r, u32 extra_bytes) {  // thread 0 only
         const u32 ba = 4u * P.za16, bb = 4u * P.zb16;
+        if (P.ready) {  // inputs still streaming in: wait for this row's chunk
+            const uint32_t *f = P.ready + r / P.ready_rows;
+            while (ld_acquire_sys(f) != P.epoch) __nanosleep(64);
+            fence_proxy_async_all();
+        }
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(mbar, ba + bb + extra_bytes);
         if (ba) bulk_g2s(stA, P.a + r * P.lda, ba, mbar);

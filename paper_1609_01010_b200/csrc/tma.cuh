@@ -63,6 +63,19 @@ __device__ __forceinline__ void tma_load_3d(void *sdst, const void *tmap, int c0
         : "memory");
 }
 
+// Acquire load at system scope (a flag written by a copy stream's
+// stream-memory operation), then order later async-proxy (bulk copy) reads
+// after it.
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void fence_proxy_async_all() {
+    asm volatile("fence.proxy.async;" ::: "memory");
+}
+
 // Bulk store shared -> global (cp.async.bulk, bulk-group completion): 16-byte
 // aligned addresses on both sides, size a multiple of 16.  Used for product
 // rows written straight to page-locked host memory (zero-copy host calls),

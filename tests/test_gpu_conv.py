@@ -186,6 +186,57 @@ def test_host_buffers_zero_copy_and_pipeline(orc, engine):
     assert np.array_equal(got.numpy().view(np.uint32), want)
 
 
+@pytest.mark.parametrize("engine", ["fft_pad", "tft"])
+def test_host_streamed_inputs(orc, monkeypatch, engine):
+    """Streamed-input host mode (operand chunks H2D on a copy stream with
+    per-chunk ready flags, one persistent kernel writing the page-locked
+    output), forced at a small size; strided host rows included."""
+    monkeypatch.setenv("MC_STREAM_IN_MIN_MB", "0")
+    p = P3
+    B, z1, z2 = 1100, 1499, 2102  # rows not a multiple of 4 words
+    a = orc.gen_u32(24, 0, 0, B, z1, p)
+    b = orc.gen_u32(24, 1, 0, B, z2, p)
+    a[-1, :] = p - 1
+    b[-1, :] = p - 1
+    want = orc.conv_batch(a, b, p, 1 if engine == "tft" else 0, threads=8)[0]
+    at = torch.from_numpy(a.view(np.int32)).pin_memory()
+    bt = torch.from_numpy(b.view(np.int32)).pin_memory()
+    got = mc.conv_batch(at, bt, p, engine=engine)
+    assert np.array_equal(got.numpy().view(np.uint32), want)
+    ap = torch.zeros((B, z1 + 9), dtype=torch.int32).pin_memory()
+    ap[:, :z1] = at
+    got = mc.conv_batch(ap[:, :z1], bt, p, engine=engine)
+    assert np.array_equal(got.numpy().view(np.uint32), want)
+
+
+def test_host_async_calls_on_two_streams(orc):
+    """Two asynchronous host-buffer calls on different caller streams, issued
+    back to back: the second must not overwrite the first's staging."""
+    from paper_1609_01010_b200 import _native
+    p = P3
+    B, z1, z2 = 600, 1500, 2100
+    n = z1 + z2 - 1
+    outs, wants = [], []
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    keep = []
+    for k, st in enumerate(streams):
+        a = orc.gen_u32(23 + k, 0, 0, B, z1, p)
+        b = orc.gen_u32(23 + k, 1, 0, B, z2, p)
+        wants.append(orc.conv_batch(a, b, p, 1, threads=8)[0])
+        ah = torch.from_numpy(a.view(np.int32)).pin_memory()
+        bh = torch.from_numpy(b.view(np.int32)).pin_memory()
+        ch = torch.empty((B, n), dtype=torch.int32).pin_memory()
+        keep += [ah, bh]
+        outs.append(ch)
+        _native.check(_native.lib().mc_conv_host_async(
+            1, ah.data_ptr(), z1, z1, bh.data_ptr(), z2, z2, ch.data_ptr(), n, B, p, 0,
+            st.cuda_stream))
+    for st in streams:
+        st.synchronize()
+    for ch, want in zip(outs, wants):
+        assert np.array_equal(ch.numpy().view(np.uint32), want)
+
+
 def test_list_api_poly_mul(golden_small):
     for c in golden_small["poly_mul"]:
         fp = mc.FourierPrime.from_modulus(c["p"])
