@@ -346,7 +346,9 @@ static int stream_in_call(PipeState &S, int engine, const uint32_t *a, int64_t l
     // 32 uniform chunks: used only for >= 512 MiB of operands, so every copy
     // is large (a copy-engine call costs ~10-20 us; geometric chunk sizes were
     // measured worse: the kernel stalls on the last, largest chunk)
-    const int64_t rows = std::max<int64_t>(16, (batch + 31) / 32);
+    const char *ce = getenv("MC_STREAM_IN_CHUNKS");  // A/B override of the chunk count
+    const int64_t want = ce && *ce ? std::max(1, atoi(ce)) : 32;
+    const int64_t rows = std::max<int64_t>(16, (batch + want - 1) / want);
     const int64_t nch = (batch + rows - 1) / rows;
     if (nch > PipeState::MAX_CHUNKS || rows > 0x7fffffff) return 1;
     auto fail_out = [&](mc_status st) { *out = st; return 0; };
