@@ -266,14 +266,19 @@ def run_mine(args, cfg):
     _native.check(lib.mc_gen_u32(cfg["seed"], 0, row0, B, z1, hi, a.data_ptr(), z1, sh))
     _native.check(lib.mc_gen_u32(cfg["seed"], 1, row0, B, z2, hi, b.data_ptr(), z2, sh))
     if engine == "three_primes" and ws > 1:
-        # one product, primes spread over the ranks, residues gathered to
-        # rank 0 for the CRT (the only collective of the path)
-        from paper_1609_01010_b200.distributed import mul_three_primes_distributed
+        # one product, primes spread over the ranks; the residues meet in the
+        # CRT: by default each rank's Garner slice reads them from the GPUs
+        # that computed them and writes rank 0's limbs over peer memory (the
+        # gather fused into the kernel); MC_CRT_NCCL=1 gathers them to rank 0
+        # with NCCL send/recv first
+        from paper_1609_01010_b200.distributed import (mul_three_primes_distributed,
+                                                       mul_three_primes_p2p)
 
         c = torch.empty((3, n), dtype=torch.int32, device=dev)
+        dist_fn = mul_three_primes_distributed if os.environ.get("MC_CRT_NCCL") else mul_three_primes_p2p
 
         def step():
-            mul_three_primes_distributed(a[0], b[0], dst=0)
+            dist_fn(a[0], b[0], dst=0)
     elif engine == "three_primes":
         c = torch.empty((3, n), dtype=torch.int32, device=dev)
 

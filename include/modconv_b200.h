@@ -137,6 +137,24 @@ mc_status mc_itft(const uint32_t *xhat, uint32_t *y, int32_t n, int32_t log2L,
 mc_status mc_crt3(const uint32_t *r1, const uint32_t *r2, const uint32_t *r3,
                   uint32_t *limbs, int64_t n, void *stream);
 
+/* A slice of the CRT: count coefficients, limbs[k*limb_stride + i].  Any
+ * pointer may address a peer GPU's memory (CUDA IPC, NVLink): the
+ * distributed three-primes path runs one slice per rank, each reading the
+ * residue vectors where they were computed and writing its limbs straight
+ * into the destination rank's buffer -- the gather fused into the kernel. */
+mc_status mc_crt3_slice(const uint32_t *r1, const uint32_t *r2, const uint32_t *r3,
+                        uint32_t *limbs, int64_t limb_stride, int64_t count, void *stream);
+
+/* Peer memory for the distributed CRT (control plane): device allocation
+ * with its 64-byte IPC handle; open / close a peer's handle; free. */
+mc_status mc_ipc_alloc(int64_t bytes, void **dptr, uint8_t *handle);
+mc_status mc_ipc_open(const uint8_t *handle, void **dptr);
+mc_status mc_ipc_close(void *dptr);
+mc_status mc_ipc_free(void *dptr);
+/* Device-to-device copy on `stream` (the destination rank copies the limbs
+ * out of its IPC-shared buffer into the caller's tensor). */
+mc_status mc_copy_device(void *dst, const void *src, int64_t bytes, void *stream);
+
 /* Three-primes integer product over Z: a (z1 words) and b (z2 words) are
  * non-negative integers < 2^32 (any width; reduced mod each prime on the
  * fly, poly.py:46-49 from_ints semantics); the exact product coefficients

@@ -2,6 +2,8 @@
 // the convolution engines (inputs reduced on load), then Garner CRT into
 // 3 x 32-bit limbs.  No reference counterpart; see
 // SURVEY.md section 8 a14 for the definition used here.
+#include <cstring>
+
 #include "fourstep.cuh"
 #include "runtime.h"
 
@@ -32,9 +34,13 @@ static CrtConsts crt_consts() {
 
 // Garner: y2 = (r2 - r1) / p1 mod p2; x12 = r1 + p1*y2 (< p1*p2);
 // y3 = (r3 - x12) / (p1*p2) mod p3; x = x12 + p1*p2*y3 (< 2^90).
+// limbs[k * ls + i] for i < n; ls = n for the planar [3][n] layout, or the
+// full length when a slice is written (the distributed CRT: residues and
+// limbs may live in peer GPUs' memory, reached over NVLink by these loads
+// and stores -- the gather is fused into the kernel).
 __global__ void crt3_kernel(const u32 *__restrict__ r1, const u32 *__restrict__ r2,
                             const u32 *__restrict__ r3, u32 *__restrict__ limbs, long long n,
-                            const CrtConsts K) {
+                            long long ls, const CrtConsts K) {
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const u32 a = __ldcs(r1 + i), b = __ldcs(r2 + i), c = __ldcs(r3 + i);
@@ -47,17 +53,18 @@ __global__ void crt3_kernel(const u32 *__restrict__ r1, const u32 *__restrict__ 
         const unsigned long long s = lo + x12;
         const unsigned long long h = hi + (s < lo ? 1ull : 0ull);
         __stcs(limbs + i, (u32)s);
-        __stcs(limbs + n + i, (u32)(s >> 32));
-        __stcs(limbs + 2 * n + i, (u32)h);
+        __stcs(limbs + ls + i, (u32)(s >> 32));
+        __stcs(limbs + 2 * ls + i, (u32)h);
     }
 }
 
 static mc_status launch_crt(const u32 *r1, const u32 *r2, const u32 *r3, u32 *limbs, long long n,
-                            cudaStream_t st) {
+                            cudaStream_t st, long long ls = -1) {
     if (n <= 0) return n == 0 ? MC_OK : fail(MC_EINVAL, "negative length");
+    if (ls < 0) ls = n;
     const int thr = 256;
     long long blocks = std::min<long long>((n + thr - 1) / thr, (long long)sm_count() * 8);
-    crt3_kernel<<<(unsigned)blocks, thr, 0, st>>>(r1, r2, r3, limbs, n, crt_consts());
+    crt3_kernel<<<(unsigned)blocks, thr, 0, st>>>(r1, r2, r3, limbs, n, ls, crt_consts());
     note_launches(1);
     MC_CUDA_CHECK(cudaGetLastError());
     return MC_OK;
@@ -77,6 +84,54 @@ mc_status mc_crt3(const uint32_t *r1, const uint32_t *r2, const uint32_t *r3, ui
                   int64_t n, void *stream) {
     if (n > 0 && (!r1 || !r2 || !r3 || !limbs)) return fail(MC_EINVAL, "null pointer");
     return launch_crt(r1, r2, r3, limbs, n, (cudaStream_t)stream);
+}
+
+mc_status mc_crt3_slice(const uint32_t *r1, const uint32_t *r2, const uint32_t *r3,
+                        uint32_t *limbs, int64_t limb_stride, int64_t count, void *stream) {
+    if (count < 0 || limb_stride < count) return fail(MC_EINVAL, "bad slice");
+    if (count > 0 && (!r1 || !r2 || !r3 || !limbs)) return fail(MC_EINVAL, "null pointer");
+    return launch_crt(r1, r2, r3, limbs, count, (cudaStream_t)stream, limb_stride);
+}
+
+// ---- peer memory for the distributed CRT (CUDA IPC; control plane only)
+mc_status mc_ipc_alloc(int64_t bytes, void **dptr, uint8_t *handle) {
+    if (bytes <= 0 || !dptr || !handle) return fail(MC_EINVAL, "bad arguments");
+    MC_CUDA_CHECK(cudaMalloc(dptr, (size_t)bytes));
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, *dptr);
+    if (e != cudaSuccess) {
+        cudaFree(*dptr);
+        *dptr = nullptr;
+        return cuda_fail(e, "cudaIpcGetMemHandle");
+    }
+    memcpy(handle, &h, sizeof(h));
+    return MC_OK;
+}
+
+mc_status mc_ipc_open(const uint8_t *handle, void **dptr) {
+    if (!handle || !dptr) return fail(MC_EINVAL, "bad arguments");
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    MC_CUDA_CHECK(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return MC_OK;
+}
+
+mc_status mc_ipc_close(void *dptr) {
+    MC_CUDA_CHECK(cudaIpcCloseMemHandle(dptr));
+    return MC_OK;
+}
+
+mc_status mc_ipc_free(void *dptr) {
+    MC_CUDA_CHECK(cudaFree(dptr));
+    return MC_OK;
+}
+
+mc_status mc_copy_device(void *dst, const void *src, int64_t bytes, void *stream) {
+    if (bytes < 0 || (bytes > 0 && (!dst || !src))) return fail(MC_EINVAL, "bad arguments");
+    if (bytes == 0) return MC_OK;
+    MC_CUDA_CHECK(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice,
+                                  (cudaStream_t)stream));
+    return MC_OK;
 }
 
 int64_t mc_three_primes_scratch_words(int32_t z1, int32_t z2) {

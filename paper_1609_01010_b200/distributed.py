@@ -3,10 +3,20 @@ torch.distributed over NCCL; gloo for CPU tests).
 
 The path shards without exchange: independent products of a batch are
 partitioned by contiguous row ranges (configs 2-4), and the three primes of
-the integer product (config 5) are spread over ranks.  The only collective
-is the gather of config 5's residue vectors onto the rank that runs the CRT
-kernel.  Nothing here is on the reference's side:
-the reference has no distributed component.
+the integer product (config 5) are spread over ranks.  The only exchange is
+config 5's residue vectors meeting in the CRT, done
+two ways:
+
+* mul_three_primes_p2p (default on GPUs): each rank's Garner kernel reads
+  the residue vectors from the GPUs that computed them and writes its slice
+  of the limbs into the destination rank's buffer, all over NVLink peer
+  memory (CUDA IPC) -- the gather fused into the CRT kernel; the process
+  group only carries the IPC handles and two barriers;
+* mul_three_primes_distributed: residues sent to the CRT rank with
+  torch.distributed send/recv (NCCL), then one CRT kernel there.
+
+Nothing here is on the reference's side: the reference has no distributed
+component.
 """
 
 from __future__ import annotations
@@ -99,3 +109,115 @@ def mul_three_primes_distributed(a: torch.Tensor, b: torch.Tensor, dst: int = 0,
     if rank != dst:
         return None
     return crt(residues[0], residues[1], residues[2])
+
+
+# ---------------------------------------------------------------- peer memory
+class _PeerCrt:
+    """IPC-shared buffers of the fused distributed CRT for one (n, dst,
+    group): every rank owns a [3][n] residue buffer (it writes the planes of
+    its primes), dst owns the [3][n] limb buffer; every rank maps all of
+    them.  Cached per shape: opening IPC handles costs milliseconds."""
+
+    def __init__(self, n: int, dst: int, group):
+        import ctypes
+
+        from . import _native
+
+        self.lib = _native.lib()
+        self.ws = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n = n
+        self._own, self._opened = [], []
+        res, h_res = self._alloc(12 * n)
+        out, h_out = (self._alloc(12 * n) if self.rank == dst else (None, None))
+        handles = [None] * self.ws
+        dist.all_gather_object(handles, (h_res, h_out), group=group)
+        self.res = [res if r == self.rank else self._open(handles[r][0]) for r in range(self.ws)]
+        self.out = out if self.rank == dst else self._open(handles[dst][1])
+        self._ctypes = ctypes
+
+    def _alloc(self, nbytes):
+        import ctypes
+
+        from . import _native
+
+        ptr = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(64)
+        _native.check(self.lib.mc_ipc_alloc(nbytes, ctypes.byref(ptr), h))
+        self._own.append(ptr.value)
+        return ptr.value, h.raw
+
+    def _open(self, handle):
+        import ctypes
+
+        from . import _native
+
+        ptr = ctypes.c_void_p()
+        _native.check(self.lib.mc_ipc_open(handle, ctypes.byref(ptr)))
+        self._opened.append(ptr.value)
+        return ptr.value
+
+    def close(self):
+        for p in self._opened:
+            self.lib.mc_ipc_close(p)
+        for p in self._own:
+            self.lib.mc_ipc_free(p)
+        self._opened, self._own = [], []
+
+
+_PEER_CACHE: dict = {}
+
+
+def close_peer_buffers(group=None) -> None:
+    """Release the cached IPC buffers (collective: call on every rank)."""
+    if dist.is_initialized():
+        dist.barrier(group=group)
+    for st in _PEER_CACHE.values():
+        st.close()
+    _PEER_CACHE.clear()
+
+
+def mul_three_primes_p2p(a: torch.Tensor, b: torch.Tensor, dst: int = 0, group=None):
+    """Exact integer product of a and b (int32 words on this rank's GPU,
+    identical on every rank), primes spread over the ranks; the residue
+    gather is fused into the CRT kernel over peer memory.
+
+    Rank r computes the residue planes of its primes (k % ws == r) into its
+    IPC-shared buffer; after a barrier every rank runs the Garner kernel on
+    its coefficient slice (shard_rows(n, ws, r)), loading the three residue
+    planes from their owners' GPUs and storing its limbs straight into
+    dst's buffer over NVLink; after a second barrier dst copies the limbs
+    out.  Returns [3, n] int32 limbs on dst, None elsewhere.
+    """
+    from . import _native, _tensors
+
+    ws = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if ws == 1:
+        from .crt import mul_three_primes_tensor
+
+        return mul_three_primes_tensor(a, b)
+    lib = _native.lib()
+    z1, z2 = a.numel(), b.numel()
+    n = z1 + z2 - 1
+    key = (n, dst, id(group), ws)
+    st = _PEER_CACHE.get(key)
+    if st is None:
+        st = _PEER_CACHE[key] = _PeerCrt(n, dst, group)
+    stream = _tensors.stream_handle()
+    a_, b_ = a.contiguous(), b.contiguous()
+    for k in primes_of_rank(ws, rank):
+        _native.check(lib.mc_mul_mod_prime_k(a_.data_ptr(), z1, b_.data_ptr(), z2,
+                                             st.res[rank] + 4 * k * n, k, stream))
+    torch.cuda.current_stream().synchronize()
+    dist.barrier(group=group)  # every residue plane is written
+    lo, cnt = shard_rows(n, ws, rank)
+    r = [st.res[k % ws] + 4 * (k * n + lo) for k in range(3)]
+    _native.check(lib.mc_crt3_slice(r[0], r[1], r[2], st.out + 4 * lo, n, cnt, stream))
+    torch.cuda.current_stream().synchronize()
+    dist.barrier(group=group)  # every limb slice is in dst's buffer
+    if rank != dst:
+        return None
+    out = torch.empty((3, n), dtype=torch.int32, device=a.device)
+    _native.check(lib.mc_copy_device(out.data_ptr(), st.out, 12 * n, stream))
+    return out
