@@ -56,6 +56,27 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_fwd
     }
 }
 
+// Final column store: rows t + G*s of column col (first n positions of the
+// product).  Only a tile that reaches position n needs the per-slot bound
+// check (tile-uniform branch); the others store through one base pointer.
+template <int KR, int KC, int NT, int AR>
+__device__ __forceinline__ void store_col(u32 *dst, const u32 (&v)[16], int t, long long col,
+                                          long long tile_col0, const FourParams &P) {
+    using C = ColCfg<KR>;
+    constexpr long long Ccols = 1ll << KC;
+    constexpr long long SLOT = (long long)C::G * Ccols;  // position stride of a slot
+    u32 *base = dst + (long long)t * Ccols + col;
+    if (15 * SLOT + (long long)(C::G - 1) * Ccols + tile_col0 + C::TC - 1 < P.n) {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) __stcs(base + s * SLOT, canon_t<(NT < 16 ? 0 : AR)>(v[s], P.cs.p));
+    } else {
+        const long long idx0 = (long long)t * Ccols + col;
+#pragma unroll
+        for (int s = 0; s < 16; ++s)
+            if (idx0 + s * SLOT < P.n) __stcs(base + s * SLOT, canon_t<(NT < 16 ? 0 : AR)>(v[s], P.cs.p));
+    }
+}
+
 // Inverse: R-point inverse DIT up each column; truncated (NT < 16): rows
 // >= NT*R/16 hold the column time values, which are zero for a product of
 // length <= NT*L/16, then the van der Hoeven top pass (ItftTop).
@@ -92,11 +113,7 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_inv
     LayCol<C::TC> lay{c};
     inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, NT, AR>(tile, v, t, P.cs, W, lay);
     inv_top<KR, NT, AR>(v, t, P.cs, W);
-#pragma unroll
-    for (int s = 0; s < 16; ++s) {
-        const long long idx = (long long)(t + C::G * s) * Ccols + col;
-        if (idx < P.n) __stcs(dst + idx, canon_t<(NT < 16 ? 0 : AR)>(v[s], P.cs.p));
-    }
+    store_col<KR, KC, NT, AR>(dst, v, t, col, (long long)blockIdx.x * C::TC, P);
 }
 
 // Forward column pass, TMA variant: persistent CTAs walk the (product,
@@ -248,11 +265,7 @@ __global__ void __launch_bounds__(1024, 1) col_inv_async_kernel(const FourParams
         inv_top<KR, NT, AR>(v, t, P.cs, W);
         u32 *dst = P.c + (P.prod0 + pc) * P.ldc;
         const long long col = (long long)ct * C::TC + c;
-#pragma unroll
-        for (int s = 0; s < 16; ++s) {
-            const long long idx = (long long)(t + C::G * s) * Ccols + col;
-            if (idx < P.n) __stcs(dst + idx, canon_t<(NT < 16 ? 0 : AR)>(v[s], P.cs.p));
-        }
+        store_col<KR, KC, NT, AR>(dst, v, t, col, (long long)ct * C::TC, P);
         k ^= 1;
     }
 }
