@@ -317,18 +317,23 @@ def run_mine(args, cfg):
         step()
     torch.cuda.synchronize()
     graph = None
-    if B * n <= (1 << 20) and engine != "three_primes":
-        # launch-bound workload (config 1): replay the step from a CUDA graph so
+    if (B * n <= (1 << 20) and engine != "three_primes") or (engine == "three_primes" and ws == 1):
+        # launch-bound workloads (config 1; config 5's ~20 launches and stream-
+        # ordered allocations per step): replay the step from a CUDA graph so
         # the timed region measures the device, not the Python launch path
         l0 = _native.launch_count()
         step()
         launches_per_step = _native.launch_count() - l0
         torch.cuda.synchronize()
+        eager_out = c.clone()
+        c.zero_()
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             step()
         graph.replay()
         torch.cuda.synchronize()
+        assert torch.equal(c, eager_out), "graph replay differs from the eager step"
+        del eager_out
         step_eager = step
 
         def step():
