@@ -30,7 +30,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
          "-Xcompiler", "-Wall", f"-I{INCLUDE}", f"-I{CSRC}"]
 SMALL_KS = range(4, 14)
-COL_KRS = range(4, 13)
+COL_KRS = range(4, 14)
 
 
 def _units():

@@ -202,6 +202,7 @@ static cudaError_t launch_cols_any(int KC, int KR, int NT, const FourParams &P, 
         case 10: return launch_cols_kr10(P, KC, NT, fwd, st, tma);
         case 11: return launch_cols_kr11(P, KC, NT, fwd, st, tma);
         case 12: return launch_cols_kr12(P, KC, NT, fwd, st, tma);
+        case 13: return launch_cols_kr13(P, KC, NT, fwd, st, tma);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -265,13 +266,11 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     int K = 0;
     while ((1ll << K) < n) ++K;
     if (circ) K = circ_log2L;
-    if (K > kFourStepMaxK)
-        return fail(MC_EUNSUPPORTED, "transform size 2^" + std::to_string(K) +
-                                         " exceeds the four-step limit 2^" +
-                                         std::to_string(kFourStepMaxK));
     const FieldTables *TL, *TR, *TC;
-    mc_status s = get_tables(p, K, &TL);
+    mc_status s = get_tables(p, K, &TL);  // the reference's 2-adicity check
     if (s != MC_OK) return s;
+    if (K > kFourStepMaxK)  // L = 2^27 (p3 only): level-scheduled transforms
+        return levels_conv(a, lda, z1, b, ldb, z2, c, ldc, batch, p, K, n, st);
     // Row length C = 2^KC: 2^12 (measured better than 2^13 at K = 23, whose
     // wider column tiles do not pay for the 1-CTA/SM K=13 row pass);
     // MC_FOURSTEP_KC overrides for A/B runs.
@@ -280,6 +279,7 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
         return e ? atoi(e) : 0;
     }();
     int KC = std::min(12, K - 4);
+    if (K - KC > 12) KC = 13;  // K = 25, 26: 2^13-point rows, 2^12 / 2^13-point columns
     if (kc_env >= 10 && kc_env <= 13 && K - kc_env >= 4 && K - kc_env <= 12 &&
         (kc_env == 12 || kc_env == 13 || K - kc_env == 4))
         KC = kc_env;

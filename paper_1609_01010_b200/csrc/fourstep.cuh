@@ -22,7 +22,14 @@
 namespace mc {
 
 // Largest K handled by the two-level (R x C) decomposition.
-constexpr int kFourStepMaxK = 24;
+constexpr int kFourStepMaxK = 26;
+
+// Products beyond the four-step limit (L = 2^27 with p3, whose 2-adicity is
+// 27): level-scheduled transforms on global memory (transforms.cu), one
+// product at a time.  Correct, not fast (~27 global passes per transform).
+mc_status levels_conv(const u32 *a, long long lda, int z1, const u32 *b, long long ldb, int z2,
+                      u32 *c, long long ldc, long long batch, u32 p, int K, long long n,
+                      cudaStream_t st);
 
 mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u32 *b,
                         long long ldb, int z2, u32 *c, long long ldc, long long batch, u32 p,

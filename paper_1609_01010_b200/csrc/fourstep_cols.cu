@@ -313,7 +313,8 @@ static cudaError_t launch_fwd_tma(const FourParams &P, const ColTma &M, cudaStre
 template <int KR, int KC, int NT, int AR = 0>
 static cudaError_t launch_one(const FourParams &P, bool fwd, cudaStream_t st,
                               const ColTma *tma) {
-    if constexpr (KR >= 6 && ColCfg<KR>::TILE == 16384) {
+    // bulk-copy / async variants need >= 16-byte tile rows (TC >= 4, KR <= 12)
+    if constexpr (KR >= 6 && ColCfg<KR>::TILE == 16384 && ColCfg<KR>::TC >= 4) {
         if (fwd && tma && tma->ok) return launch_fwd_tma<KR, KC, NT, AR>(P, *tma, st);
         if (!fwd && col_inv_async_on()) return launch_inv_async<KR, KC, NT, AR>(P, st);
     }
@@ -370,12 +371,15 @@ cudaError_t MC_CAT(launch_cols_kr, MC_KR)(const FourParams &P, int KC, int NT, b
         case 12: return launch_nt<4, 12>(P, NT, fwd, st, tma);
         default: return cudaErrorInvalidValue;
     }
-#elif MC_KR >= 9 && MC_KR <= 11
-    switch (KC) {  // K = 21..24 may use 2^13 rows
+#elif MC_KR >= 9 && MC_KR <= 12
+    switch (KC) {  // K = 21..25 may use 2^13 rows (K = 25 always does)
         case 12: return launch_nt<MC_KR, 12>(P, NT, fwd, st, tma);
         case 13: return launch_nt<MC_KR, 13>(P, NT, fwd, st, tma);
         default: return cudaErrorInvalidValue;
     }
+#elif MC_KR == 13
+    if (KC != 13) return cudaErrorInvalidValue;  // K = 26
+    return launch_nt<13, 13>(P, NT, fwd, st, tma);
 #else
     if (KC != 12) return cudaErrorInvalidValue;
     return launch_nt<MC_KR, 12>(P, NT, fwd, st, tma);

@@ -100,6 +100,8 @@ cudaError_t launch_cols_kr11(const FourParams &P, int KC, int NT, bool fwd, cuda
                              const ColTma *tma = nullptr);
 cudaError_t launch_cols_kr12(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st,
                              const ColTma *tma = nullptr);
+cudaError_t launch_cols_kr13(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st,
+                             const ColTma *tma = nullptr);
 
 template <class KF>
 static cudaError_t prep_kernel(KF kern, int smem, int threads, int *per_sm) {

@@ -220,6 +220,54 @@ static mc_status tfm_setup(u32 p, int K, TfmParams *P) {
     return MC_OK;
 }
 
+__global__ void pointwise_kernel(u32 *x, const u32 *y, long long L, TfmParams P) {
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < L;
+         i += (long long)gridDim.x * blockDim.x)
+        x[i] = mulv(x[i], y[i], P);
+}
+
+mc_status levels_conv(const u32 *a, long long lda, int z1, const u32 *b, long long ldb, int z2,
+                      u32 *c, long long ldc, long long batch, u32 p, int K, long long n,
+                      cudaStream_t st) {
+    TfmParams P;
+    memset(&P, 0, sizeof(P));
+    mc_status s = tfm_setup(p, K, &P);
+    if (s != MC_OK || batch == 0) return s;
+    const long long L = 1ll << K;
+    const u32 red_wp = (u32)((1ull << 32) / p);
+    u32 *buf = nullptr;
+    keep_pool_memory();
+    MC_CUDA_CHECK(cudaMallocAsync(&buf, 4ull * 3 * L, st));
+    u32 *wa = buf, *wb = buf + L, *tmp = buf + 2 * L;
+    P.ldw = L;
+    P.batch = 1;
+    const FieldTables *T;
+    get_tables(p, K, &T);
+    auto forward = [&](const u32 *x, long long ldx, long long z, u32 *w) {
+        // zero-padded, reduced copy, then the bit-reversed DIT = natural-order spectrum
+        load_pad_kernel<<<grid_for(L), 256, 0, st>>>(x, ldx, z, tmp, L, L, 1, p, red_wp);
+        bitrev_copy_kernel<<<grid_for(L), 256, 0, st>>>(tmp, w, L, 1, K);
+        P.w = w;
+        for (long long h = 1; h < L; h <<= 1)
+            dit_stage_kernel<<<grid_for(L / 2), 256, 0, st>>>(P, h, 0);
+    };
+    for (long long r = 0; r < batch; ++r) {
+        forward(a + r * lda, lda, z1, wa);
+        forward(b + r * ldb, ldb, z2, wb);
+        pointwise_kernel<<<grid_for(L), 256, 0, st>>>(wa, wb, L, P);
+        bitrev_copy_kernel<<<grid_for(L), 256, 0, st>>>(wa, tmp, L, 1, K);
+        P.w = tmp;
+        for (long long h = 1; h < L; h <<= 1)
+            dit_stage_kernel<<<grid_for(L / 2), 256, 0, st>>>(P, h, 1);
+        scale_copy_kernel<<<grid_for(n), 256, 0, st>>>(tmp, L, c + r * ldc, n, ldc, 1, T->linv.w,
+                                                       T->linv.wp, p, 1);
+        note_launches(8 + 3 * K);
+    }
+    cudaFreeAsync(buf, st);
+    MC_CUDA_CHECK(cudaGetLastError());
+    return MC_OK;
+}
+
 }  // namespace mc
 
 using namespace mc;

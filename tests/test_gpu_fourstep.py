@@ -136,3 +136,45 @@ def test_fourstep_truncated_large(orc, z1, z2):
     want, _, _ = orc.conv_batch(to_u32_np(a), to_u32_np(b), p, orc.ENGINE_FFT_PAD)
     assert np.array_equal(to_u32_np(c), want)
     assert torch.equal(c, mc.conv_batch(a, b, p, engine="fft_pad"))
+
+
+def test_beyond_2_24_vs_oracle(orc):
+    """L = 2^25 (four-step with 2^13-point rows and 2^12-point columns), p1
+    (2-adicity 26): bit-exact against the oracle, both engines."""
+    p = P1
+    z1, z2 = (1 << 24) + 1, 1 << 23
+    a = orc.gen_u32(61, 0, 0, 1, z1, p)
+    b = orc.gen_u32(61, 1, 0, 1, z2, p)
+    a[0, :5] = p - 1
+    b[0, -5:] = p - 1
+    want, _, _ = orc.conv_batch(a, b, p)
+    at = torch.from_numpy(a.view(np.int32)).cuda()
+    bt = torch.from_numpy(b.view(np.int32)).cuda()
+    for eng in ("fft_pad", "tft"):
+        got = to_u32_np(mc.conv_batch(at, bt, p, engine=eng))
+        assert np.array_equal(got, want), eng
+
+
+@pytest.mark.parametrize("K,p", [(26, P1), (26, P3), (27, P3)])
+def test_up_to_the_two_adicity(K, p):
+    """L = 2^26 (four-step, 2^13 x 2^13) and 2^27 (level-scheduled fallback,
+    p3 only) up to each prime's 2-adicity: evaluation identity at two points
+    (the reference raises UnsupportedSizeError only beyond the 2-adicity)."""
+    z1 = (1 << (K - 1)) + 3
+    z2 = (1 << (K - 1)) - 7
+    a = gen_device(62 + K, 0, 0, 1, z1, p)
+    b = gen_device(62 + K, 1, 0, 1, z2, p)
+    c = mc.conv_batch(a, b, p, engine="fft_pad")
+    assert c.shape == (1, z1 + z2 - 1)
+    for x in (3, 123456789):
+        assert eval_vec(c, x, p) == eval_vec(a, x, p) * eval_vec(b, x, p) % p
+    del c
+    torch.cuda.empty_cache()
+
+
+def test_beyond_the_two_adicity_raises():
+    p = P2  # 2-adicity 23
+    a = gen_device(70, 0, 0, 1, (1 << 22) + 1, p)
+    with pytest.raises(mc.UnsupportedSizeError) as ei:
+        mc.conv_batch(a, a, p)
+    assert ei.value.required_two_adicity == 24
