@@ -24,7 +24,6 @@ cudaError_t launch_conv_small_k11(const ConvSmallParams &, int, cudaStream_t);
 cudaError_t launch_conv_small_k12(const ConvSmallParams &, int, cudaStream_t);
 cudaError_t launch_conv_small_k13(const ConvSmallParams &, int, cudaStream_t);
 
-static const int kSmallMaxK = 13;
 
 // ---------------------------------------------------------------- tiny sizes
 // L <= 8: one thread per product, direct convolution with 64-bit

@@ -40,6 +40,9 @@
 
 namespace mc {
 
+// Largest transform size of the fused single-CTA kernels (L = 2^13).
+constexpr int kSmallMaxK = 13;
+
 struct ConvSmallParams {
     const u32 *a;
     const u32 *b;

@@ -2,6 +2,7 @@
 // (compiled once per K with -DMC_K=<K> so the 10 sizes build in parallel).
 #include "conv_small.cuh"
 #include "runtime.h"
+#include "xform_small.cuh"
 
 #ifndef MC_K
 #error "compile with -DMC_K=<log2 L>"
@@ -51,6 +52,46 @@ cudaError_t MC_CAT(launch_conv_small_k, MC_K)(const ConvSmallParams &P, int nt, 
         case 14: return launch_nt<14, 2>(P, st);
         case 15: return launch_nt<15, 2>(P, st);
         case 16: return P.ar == 1 ? launch_nt<16, 1>(P, st) : launch_nt<16, 2>(P, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+// ---- standalone transforms (xform_small.cuh)
+template <int MODE, int NT>
+static cudaError_t launch_xf(const XformParams &X, cudaStream_t st) {
+    using C = SmallCfg<MC_K>;
+    auto kern = xform_small_kernel<MC_K, MODE, NT>;
+    const int smem = C::L * 8 + C::PPC * C::L * 4;
+    static int per_sm = 0;  // benign race: idempotent
+    if (!per_sm) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        int nb = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, C::THREADS, smem);
+        if (e != cudaSuccess) return e;
+        per_sm = nb > 0 ? nb : 1;
+    }
+    long long grid = (X.batch + C::PPC - 1) / C::PPC;
+    const long long cap = (long long)per_sm * sm_count();
+    if (grid > cap) grid = cap;
+    if (grid < 1) grid = 1;
+    kern<<<(unsigned)grid, C::THREADS, smem, st>>>(X);
+    return cudaGetLastError();
+}
+
+cudaError_t MC_CAT(launch_xform_small_k, MC_K)(const XformParams &X, int mode, int nt,
+                                               cudaStream_t st) {
+    if (mode == MODE_NTT_FWD) return launch_xf<MODE_NTT_FWD, 16>(X, st);
+    if (mode == MODE_NTT_INV) return launch_xf<MODE_NTT_INV, 16>(X, st);
+    switch (nt) {
+        case 9: return launch_xf<MODE_TFT, 9>(X, st);
+        case 10: return launch_xf<MODE_TFT, 10>(X, st);
+        case 11: return launch_xf<MODE_TFT, 11>(X, st);
+        case 12: return launch_xf<MODE_TFT, 12>(X, st);
+        case 13: return launch_xf<MODE_TFT, 13>(X, st);
+        case 14: return launch_xf<MODE_TFT, 14>(X, st);
+        case 15: return launch_xf<MODE_TFT, 15>(X, st);
+        case 16: return launch_xf<MODE_TFT, 16>(X, st);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -15,6 +15,7 @@
 
 #include "fourstep.cuh"
 #include "runtime.h"
+#include "xform_small.cuh"
 
 namespace mc {
 
@@ -268,6 +269,70 @@ mc_status levels_conv(const u32 *a, long long lda, int z1, const u32 *b, long lo
     return MC_OK;
 }
 
+// ---------------------------------------------------------------- fused (L <= 8192)
+// MC_XFORM_LEVELS (non-empty) forces the level-scheduled kernels (A/B, parity).
+static bool xform_levels_forced() {
+    static const bool on = [] { const char *e = getenv("MC_XFORM_LEVELS"); return e && *e; }();
+    return on;
+}
+
+cudaError_t launch_xform_small_k4(const XformParams &, int, int, cudaStream_t);
+cudaError_t launch_xform_small_k5(const XformParams &, int, int, cudaStream_t);
+cudaError_t launch_xform_small_k6(const XformParams &, int, int, cudaStream_t);
+cudaError_t launch_xform_small_k7(const XformParams &, int, int, cudaStream_t);
+cudaError_t launch_xform_small_k8(const XformParams &, int, int, cudaStream_t);
+cudaError_t launch_xform_small_k9(const XformParams &, int, int, cudaStream_t);
+cudaError_t launch_xform_small_k10(const XformParams &, int, int, cudaStream_t);
+cudaError_t launch_xform_small_k11(const XformParams &, int, int, cudaStream_t);
+cudaError_t launch_xform_small_k12(const XformParams &, int, int, cudaStream_t);
+cudaError_t launch_xform_small_k13(const XformParams &, int, int, cudaStream_t);
+
+// Fused single-CTA transform (xform_small.cuh); K in [4, kSmallMaxK].
+static mc_status xform_small(int mode, const u32 *x, long long ldx, int z, u32 *y, long long ldy,
+                             int n, int K, long long batch, u32 p, cudaStream_t st) {
+    const FieldTables *T;
+    mc_status s = get_tables(p, K, &T);
+    if (s != MC_OK) return s;
+    XformParams X;
+    memset(&X, 0, sizeof(X));
+    X.cs.p = p;
+    X.cs.pinv = T->pinv;
+    X.cs.tf = T->tf;
+    X.cs.ti = T->ti;
+    memcpy(X.cs.c16f, T->h16f, sizeof(X.cs.c16f));
+    memcpy(X.cs.c16i, T->h16i, sizeof(X.cs.c16i));
+    memcpy(X.cs.mlev, T->mlev, sizeof(X.cs.mlev));
+    memcpy(X.cs.hinv, T->hinv, sizeof(X.cs.hinv));
+    X.x = x;
+    X.ldx = ldx;
+    X.y = y;
+    X.ldy = ldy;
+    X.z = z;
+    X.n = n;
+    X.batch = batch;
+    X.linv = T->linv;
+    X.red_wp = (u32)((1ull << 32) / p);
+    const int G = 1 << (K - 4);
+    const int nt = (n + G - 1) / G;
+    cudaError_t e;
+    switch (K) {
+        case 4: e = launch_xform_small_k4(X, mode, nt, st); break;
+        case 5: e = launch_xform_small_k5(X, mode, nt, st); break;
+        case 6: e = launch_xform_small_k6(X, mode, nt, st); break;
+        case 7: e = launch_xform_small_k7(X, mode, nt, st); break;
+        case 8: e = launch_xform_small_k8(X, mode, nt, st); break;
+        case 9: e = launch_xform_small_k9(X, mode, nt, st); break;
+        case 10: e = launch_xform_small_k10(X, mode, nt, st); break;
+        case 11: e = launch_xform_small_k11(X, mode, nt, st); break;
+        case 12: e = launch_xform_small_k12(X, mode, nt, st); break;
+        case 13: e = launch_xform_small_k13(X, mode, nt, st); break;
+        default: return fail(MC_EINVAL, "fused transform size");
+    }
+    note_launches(1);
+    if (e != cudaSuccess) return cuda_fail(e, "fused transform launch");
+    return MC_OK;
+}
+
 }  // namespace mc
 
 using namespace mc;
@@ -285,6 +350,9 @@ mc_status mc_ntt(const uint32_t *x, uint32_t *y, int32_t log2L, int64_t batch, u
     if (!x || !y) return fail(MC_EINVAL, "null pointer");
     cudaStream_t st = (cudaStream_t)stream;
     const long long L = 1ll << log2L;
+    if (log2L >= 4 && log2L <= kSmallMaxK && !xform_levels_forced())
+        return xform_small(inverse ? MODE_NTT_INV : MODE_NTT_FWD, x, L, (int)L, y, L, (int)L,
+                           log2L, batch, p, st);
     u32 *w = nullptr;
     keep_pool_memory();
     MC_CUDA_CHECK(cudaMallocAsync(&w, 4ull * L * batch, st));
@@ -318,6 +386,8 @@ mc_status mc_tft(const uint32_t *x, int32_t z, uint32_t *y, int32_t n, int32_t l
     if (s != MC_OK || batch == 0) return s;
     if (!x || !y) return fail(MC_EINVAL, "null pointer");
     cudaStream_t st = (cudaStream_t)stream;
+    if (log2L >= 4 && log2L <= kSmallMaxK && 2ll * n > L && !xform_levels_forced())
+        return xform_small(MODE_TFT, x, z, z, y, n, n, log2L, batch, p, st);
     u32 *w = nullptr;
     keep_pool_memory();
     MC_CUDA_CHECK(cudaMallocAsync(&w, 4ull * L * batch, st));

@@ -104,6 +104,36 @@ def test_large_transforms_vs_oracle(orc, lg):
     assert back == orc.itft(np.array(y, dtype=np.uint32), L, p)[0].tolist()
 
 
+@pytest.mark.parametrize("lg", list(range(4, 14)))
+@pytest.mark.parametrize("p", [P1, P3])
+def test_fused_transforms_every_size(orc, lg, p):
+    """The fused single-CTA transforms (L = 16 .. 8192): batched moddft both
+    ways and tft at several (n, z) against the oracle, all-(p-1) rows
+    included."""
+    L = 1 << lg
+    B = 5
+    x = orc.gen_u32(63, 0, lg, B, L, p)
+    x[2, :] = p - 1
+    sh = _tensors.stream_handle()
+    xt = torch.from_numpy(x.view(np.int32)).cuda()
+    y = torch.empty_like(xt)
+    _native.check(_native.lib().mc_ntt(xt.data_ptr(), y.data_ptr(), lg, B, p, 0, sh))
+    fwd = y.cpu().numpy().view(np.uint32)
+    for r in (0, 2, 4):
+        assert np.array_equal(fwd[r], orc.moddft(x[r], p)[0]), (L, r)
+    back = torch.empty_like(xt)
+    _native.check(_native.lib().mc_ntt(y.data_ptr(), back.data_ptr(), lg, B, p, 1, sh))
+    assert np.array_equal(back.cpu().numpy().view(np.uint32), x)
+    for n in sorted({L // 2 + 1, L - L // 5, L - 1, L}):
+        for z in sorted({1, n // 3 + 1, n}):
+            xz = torch.from_numpy(np.ascontiguousarray(x[:, :z]).view(np.int32)).cuda()
+            t = torch.empty((B, n), dtype=torch.int32, device="cuda")
+            _native.check(_native.lib().mc_tft(xz.data_ptr(), z, t.data_ptr(), n, lg, B, p, sh))
+            got = t.cpu().numpy().view(np.uint32)
+            for r in (1, 2):
+                assert np.array_equal(got[r], orc.tft(x[r, :z], n, L, p)[0]), (L, n, z, r)
+
+
 def test_usage_errors():
     t = _tab(257, 8)
     with pytest.raises(ValueError):
