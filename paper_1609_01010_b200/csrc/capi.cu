@@ -218,40 +218,15 @@ mc_status mc_circ_conv(const uint32_t *u, const uint32_t *v, uint32_t *w, int32_
 }
 
 // ---------------------------------------------------------------- host-buffer call
-struct HostBufs {
-    void *d = nullptr;
-    size_t bytes = 0;
-    int dev = -1;
-    ~HostBufs() {
-        if (d) cudaFree(d);
-    }
-};
-
 mc_status mc_conv_host(int engine, const uint32_t *a, int64_t lda, int32_t z1,
                        const uint32_t *b, int64_t ldb, int32_t z2, uint32_t *c, int64_t ldc,
                        int64_t batch, uint32_t p) {
-    static thread_local HostBufs buf;
-    if (engine != 0 && engine != 1) return fail(MC_EINVAL, "engine must be 0 (fft_pad) or 1 (tft)");
-    if (z1 < 1 || z2 < 1) return fail(MC_EINVAL, "inputs must be nonempty");
-    const int64_t n = (int64_t)z1 + z2 - 1;
-    if (lda < z1 || ldb < z2 || ldc < n) return fail(MC_EINVAL, "bad leading dimension");
-    if (batch <= 0) return batch == 0 ? MC_OK : fail(MC_EINVAL, "negative batch");
-    const size_t need = 4ull * batch * (z1 + z2 + n);
-    int dev = current_device();
-    if (buf.bytes < need || buf.dev != dev) {
-        if (buf.d) cudaFree(buf.d);
-        buf.d = nullptr;
-        buf.bytes = 0;
-        MC_CUDA_CHECK(cudaMalloc(&buf.d, need));
-        buf.bytes = need;
-        buf.dev = dev;
-    }
-    uint32_t *da = (uint32_t *)buf.d, *db = da + batch * z1, *dc = db + batch * z2;
-    MC_CUDA_CHECK(cudaMemcpy2D(da, 4 * z1, a, 4 * lda, 4 * z1, batch, cudaMemcpyHostToDevice));
-    MC_CUDA_CHECK(cudaMemcpy2D(db, 4 * z2, b, 4 * ldb, 4 * z2, batch, cudaMemcpyHostToDevice));
-    mc_status s = conv_dispatch(engine, da, z1, z1, db, z2, z2, dc, n, batch, p, 0);
+    // the asynchronous host path on the legacy default stream, then a
+    // synchronize: zero copy for page-locked buffers, the chunked copy
+    // pipeline for pageable ones (a ctypes caller's arrays)
+    mc_status s = mc_conv_host_async(engine, a, lda, z1, b, ldb, z2, c, ldc, batch, p, 0, nullptr);
     if (s != MC_OK) return s;
-    MC_CUDA_CHECK(cudaMemcpy2D(c, 4 * ldc, dc, 4 * n, 4 * n, batch, cudaMemcpyDeviceToHost));
+    MC_CUDA_CHECK(cudaStreamSynchronize(nullptr));
     return MC_OK;
 }
 
