@@ -167,12 +167,25 @@ def default_planner():
 
 # ------------------------------------------------------------------ list API
 def _run_lists(engine: str, u, v, req: ConvRequest) -> list[int]:
+    """One product from Python lists: residues into page-locked staging, the
+    zero-copy host call (the kernel reads and writes the staging directly),
+    the product read back as ints."""
     fp = as_field(req.field)
-    dev = _tensors.require_cuda()
-    a = _tensors.list_to_device(u, fp.p, dev).unsqueeze(0)
-    b = _tensors.list_to_device(v, fp.p, dev).unsqueeze(0)
-    c = conv_batch(a, b, fp, engine=engine)
-    return _tensors.device_to_list(c[0])
+    _tensors.require_cuda()
+    z1, z2 = len(u), len(v)
+    n = z1 + z2 - 1
+    oa, ob = 0, (z1 + 3) & ~3  # 16-byte aligned operand rows (bulk copies)
+    oc = ob + ((z2 + 3) & ~3)
+    st = _tensors.host_stage(oc + n)
+    st[oa:oa + z1] = _tensors.words_from_list(u, fp.p)
+    st[ob:ob + z2] = _tensors.words_from_list(v, fp.p)
+    base = st.ctypes.data
+    stream = torch.cuda.current_stream()
+    _native.check(_native.lib().mc_conv_host_async(
+        1 if engine == "tft" else 0, base + 4 * oa, z1, z1, base + 4 * ob, z2, z2,
+        base + 4 * oc, n, 1, fp.p, 0, int(stream.cuda_stream)))
+    stream.synchronize()
+    return st[oc:oc + n].tolist()
 
 
 def circ_conv_fft(u, v, req: ConvRequest) -> list[int]:
@@ -342,7 +355,8 @@ def poly_mul(a, b, req: ConvRequest) -> DensePoly:
         out = circ_conv_split(up, vp, req)[:out_len]
     else:
         raise ValueError(f"unknown engine {engine!r}")
-    return DensePoly(fp, tuple(out)).normalize()
+    # the engines return canonical residues: wrap without re-validating them
+    return DensePoly._trusted(fp, tuple(out)).normalize()
 
 
 def _trim(coeffs) -> list[int]:

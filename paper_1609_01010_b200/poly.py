@@ -37,6 +37,15 @@ class DensePoly:
                 raise ValueError(f"coefficient {c} out of range for p={p}")
 
     @classmethod
+    def _trusted(cls, fp: FourierPrime, coeffs: tuple) -> "DensePoly":
+        """Wrap coefficients already known to be canonical residues (engine
+        outputs) without the per-coefficient range check."""
+        obj = object.__new__(cls)
+        object.__setattr__(obj, "field", fp)
+        object.__setattr__(obj, "coeffs", coeffs)
+        return obj
+
+    @classmethod
     def from_ints(cls, field, values) -> "DensePoly":
         """Reduce arbitrary integers mod p (poly.py:46-49)."""
         fp = as_field(field)
