@@ -447,9 +447,15 @@ struct SmallCfg {
     static constexpr int SMEM = 2 * L * 8 + PPC * 2 * L * 4;
 };
 
+// Compile-time feature flags of a launch (FL): the device-resident path
+// (FL = 0) carries none of the host-I/O or input-reduction code, which costs
+// registers and scheduling freedom in the butterfly stream.
+constexpr int FL_HOST = 1;    // bulk-store epilogue / streamed-input ready flags (zero copy)
+constexpr int FL_REDUCE = 2;  // operands are arbitrary words: reduce mod p on load
+
 // Persistent kernel: each CTA copies the (p, L) stage tables into shared
 // memory once and then walks the batch with a grid stride.
-template <int K, int NT, int AR = 0>
+template <int K, int NT, int AR = 0, int FL = 0>
 __global__ void __launch_bounds__(SmallCfg<K>::THREADS, SmallCfg<K>::MINB)
 conv_small_kernel(const ConvSmallParams P) {
     static_assert(AR != 1 || NT == 16, "Harvey ranges only for complete transforms");
@@ -481,7 +487,7 @@ conv_small_kernel(const ConvSmallParams P) {
     u32 *stB = stA + P.za16;
     auto prefetch = [&](long long r, u32 extra_bytes) {  // thread 0 only
         const u32 ba = 4u * P.za16, bb = 4u * P.zb16;
-        if (P.ready) {  // inputs still streaming in: wait for this row's chunk
+        if ((FL & FL_HOST) && P.ready) {  // inputs still streaming in: wait for this row's chunk
             const uint32_t *f = P.ready + r / P.ready_rows;
             while (ld_acquire_sys(f) != P.epoch) __nanosleep(64);
             fence_proxy_async_all();
@@ -539,7 +545,7 @@ conv_small_kernel(const ConvSmallParams P) {
                 vb[s] = (valid && x < P.z2) ? __ldcs(gb + x) : 0u;
             }
         }
-        if (P.reduce) {  // three-primes inputs: any 32-bit word -> residue
+        if ((FL & FL_REDUCE) && P.reduce) {  // three-primes inputs: any 32-bit word -> residue
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 va[s] = mul_t<AR>(va[s], 1u, P.red_wp, P.p);
@@ -551,7 +557,7 @@ conv_small_kernel(const ConvSmallParams P) {
         fwd_top<K, NT, AR>(vb, P.z2, t, P, W);
         // the previous product's bulk store has read its staging before the
         // first exchange (after the barrier inside the chain) reuses bufA
-        if (C::PPC == 1 && P.bulk_out && threadIdx.x == 0) bulk_wait_read_all();
+        if ((FL & FL_HOST) && C::PPC == 1 && P.bulk_out && threadIdx.x == 0) bulk_wait_read_all();
         fwd_lower_chain<K, NT, 0, AR>(bufA, bufB, va, vb, t, P, W);
 
         // pointwise product in the last pass's layout, L^-1 folded in
@@ -583,7 +589,7 @@ conv_small_kernel(const ConvSmallParams P) {
         inv_lower_chain<K, NT, Plan<K>::NP - 1, AR>(bufA, va, t, P, W);
         inv_top<K, NT, AR>(va, t, P, W);
 
-        if (C::PPC == 1 && P.bulk_out) {
+        if ((FL & FL_HOST) && C::PPC == 1 && P.bulk_out) {
             // Stage the row in bufA (idle after the last inverse exchange; up to
             // 3 words spill into bufB, idle too) at the destination's offset mod
             // 16 bytes, then one bulk store of the aligned interior; the <= 3
@@ -614,7 +620,7 @@ conv_small_kernel(const ConvSmallParams P) {
             }
         }
     }
-    if (C::PPC == 1 && P.bulk_out && threadIdx.x == 0) bulk_wait_all();
+    if ((FL & FL_HOST) && C::PPC == 1 && P.bulk_out && threadIdx.x == 0) bulk_wait_all();
 }
 
 }  // namespace mc

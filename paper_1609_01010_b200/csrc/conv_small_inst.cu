@@ -10,10 +10,10 @@
 
 namespace mc {
 
-template <int NT, int AR>
-static cudaError_t launch_nt(const ConvSmallParams &P, cudaStream_t st) {
+template <int NT, int AR, int FL>
+static cudaError_t launch_nt_fl(const ConvSmallParams &P, cudaStream_t st) {
     using C = SmallCfg<MC_K>;
-    auto kern = conv_small_kernel<MC_K, NT, AR>;
+    auto kern = conv_small_kernel<MC_K, NT, AR, FL>;
     // dynamic shared memory: tables + data (+ TMA staging of both rows)
     const int smem = C::SMEM + (P.tma ? 16 + 4 * (P.za16 + P.zb16) : 0);
     static int attr_smem = 0, per_sm = 0, per_sm_smem = -1;  // benign races: idempotent
@@ -37,6 +37,25 @@ static cudaError_t launch_nt(const ConvSmallParams &P, cudaStream_t st) {
     if (grid < 1) grid = 1;
     kern<<<(unsigned)grid, C::THREADS, smem, st>>>(P);
     return cudaGetLastError();
+}
+
+// Feature flags: host I/O only where the bulk-copy paths exist (one product
+// per CTA); the input reduction only on complete transforms (three primes).
+template <int NT, int AR>
+static cudaError_t launch_nt(const ConvSmallParams &P, cudaStream_t st) {
+    constexpr bool one_per_cta = SmallCfg<MC_K>::PPC == 1;
+    if (P.reduce) {
+        if constexpr (NT == 16) {
+            if (P.bulk_out || P.ready) return cudaErrorInvalidValue;
+            return launch_nt_fl<NT, AR, FL_REDUCE>(P, st);
+        } else {
+            return cudaErrorInvalidValue;
+        }
+    }
+    if constexpr (one_per_cta) {
+        if (P.bulk_out || P.ready) return launch_nt_fl<NT, AR, FL_HOST>(P, st);
+    }
+    return launch_nt_fl<NT, AR, 0>(P, st);
 }
 
 #define MC_CAT2(a, b) a##b
