@@ -277,10 +277,17 @@ static std::mutex g_pipe_mu;
 //   1  streamed inputs + zero-copy output (stream_in_call): one-product-per-
 //      CTA sizes with >= 512 MiB of operands (large copy-engine chunks);
 //   0  chunked copy pipeline (other sizes).
+// MC_HOST_MODE=zc|in|pipe forces a mode where the size allows it (tests, A/B).
 static int zero_copy_shape(int64_t n, int64_t z12, int64_t batch) {
     int K = 0;
     while ((1ll << K) < n) ++K;
     if (K < 4 || K > kSmallMaxK) return 0;
+    const char *m = getenv("MC_HOST_MODE");  // read per call
+    if (m && *m) {
+        if (!strcmp(m, "zc")) return 2;
+        if (!strcmp(m, "in")) return K >= 11 ? 1 : 0;
+        return 0;
+    }
     if (8 * n * batch < (8ll << 20)) return 2;
     if (K < 11) return 0;
     const char *e = getenv("MC_STREAM_IN_MIN_MB");  // read per call (tests force the mode)

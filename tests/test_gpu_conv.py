@@ -209,6 +209,33 @@ def test_host_streamed_inputs(orc, monkeypatch, engine):
     assert np.array_equal(got.numpy().view(np.uint32), want)
 
 
+@pytest.mark.parametrize("mode", ["zc", "in", "pipe"])
+def test_host_modes_forced(orc, monkeypatch, mode):
+    """Every host mode (zero copy, streamed inputs, chunked pipeline) forced
+    on the same batch: bit-exact products, strided rows in and out, nothing
+    written past n, staging reused across calls."""
+    monkeypatch.setenv("MC_HOST_MODE", mode)
+    p = P3
+    B, z1, z2 = 1000, 1499, 2102
+    n = z1 + z2 - 1
+    a = orc.gen_u32(25, 0, 0, B, z1, p)
+    b = orc.gen_u32(25, 1, 0, B, z2, p)
+    a[0, :] = p - 1
+    b[0, :] = p - 1
+    want = orc.conv_batch(a, b, p, 1, threads=8)[0]
+    at = torch.from_numpy(a.view(np.int32)).pin_memory()
+    bt = torch.from_numpy(b.view(np.int32)).pin_memory()
+    got = mc.conv_batch(at, bt, p, engine="tft")
+    assert np.array_equal(got.numpy().view(np.uint32), want), mode
+    cp = torch.full((B, n + 3), -1, dtype=torch.int32).pin_memory()
+    ap = torch.zeros((B, z1 + 9), dtype=torch.int32).pin_memory()
+    ap[:, :z1] = at
+    for rep in range(2):  # reused staging buffers and counters
+        mc.conv_batch(ap[:, :z1], bt, p, engine="tft", out=cp[:, :n])
+        assert np.array_equal(cp[:, :n].numpy().view(np.uint32), want), (mode, rep)
+        assert (cp[:, n:] == -1).all()
+
+
 def test_host_async_calls_on_two_streams(orc):
     """Two asynchronous host-buffer calls on different caller streams, issued
     back to back: the second must not overwrite the first's staging."""
