@@ -22,7 +22,13 @@ struct RowCfg {
 };
 
 // AR: arithmetic mode (modarith.cuh); inputs and outputs in [0, 2p).
-template <int KC, int AR = 0>
+// TT: twist factors read from the precomputed per-(p, L) tables P.twf / P.twi
+// (one Shoup product per element and direction, L^-1 folded into the inverse
+// table) instead of formed as alpha_t * beta_s (two products per element and
+// direction plus the pointwise scale).  Work items are then row-major over
+// the chunk's products (item = r * chunk + product), so the CTAs working on
+// the same row r at the same time share its table row in L2.
+template <int KC, int AR = 0, bool TT = false>
 __global__ void __launch_bounds__(RowCfg<KC>::THREADS, RowCfg<KC>::THREADS >= 512 ? 1 : 2)
 row_conv_kernel(const FourParams P, int KR) {
     using RC = RowCfg<KC>;
@@ -53,6 +59,39 @@ row_conv_kernel(const FourParams P, int KR) {
          base += (long long)gridDim.x * RC::PPC) {
         const long long gr = base + grp;
         const bool valid = gr < rows;
+        if constexpr (TT) {
+            const long long prod = valid ? gr % P.chunk : 0;
+            const long long r = valid ? gr / P.chunk : 0;
+            u32 *rowA = P.Ah + prod * (R << KC) + (r << KC);
+            const u32 *rowB = P.Bh + prod * (R << KC) + (r << KC);
+            const uint2 *twf = P.twf + (r << KC);
+            const uint2 *twi = P.twi + (r << KC);
+            u32 va[16], vb[16];
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const int x = t + G * s;
+                const uint2 w = __ldg(twf + x);
+                va[s] = mul_t<AR>(valid ? rowA[x] : 0u, w.x, w.y, p);
+                vb[s] = mul_t<AR>(valid ? rowB[x] : 0u, w.x, w.y, p);
+            }
+            fwd_top<KC, 16, AR>(va, Cn, t, P.cs, W);
+            fwd_top<KC, 16, AR>(vb, Cn, t, P.cs, W);
+            fwd_lower_chain<KC, 16, 0, AR>(bufA, bufB, va, vb, t, P.cs, W);
+#pragma unroll
+            for (int s = 0; s < 16; ++s) va[s] = mont_mul(va[s], vb[s], p, P.cs.pinv);
+            inv_lower_chain<KC, 16, Plan<KC>::NP - 1, AR>(bufA, va, t, P.cs, W);
+            ItftTop<KC, 16, 16, 0, AR>::run(va, t, P.cs, W);
+            if (valid) {
+#pragma unroll
+                for (int s = 0; s < 16; ++s) {
+                    const int x = t + G * s;
+                    const uint2 w = __ldg(twi + x);  // w^-(x f1) * L^-1 * 2^32
+                    rowA[x] = mul_inv_t<AR>(va[s], w.x, w.y, p);
+                }
+            }
+            __syncthreads();
+            continue;
+        }
         const long long prod = valid ? gr / P.nrows : 0;
         const u32 r = valid ? (u32)(gr % P.nrows) : 0u;
         const u32 f1 = __brev(r) >> (32 - KR);
@@ -157,6 +196,77 @@ static mc_status get_twist(const FieldTables *T, TwistTabs *out) {
     return MC_OK;
 }
 
+// Full twist tables for the row pass (FourParams::twf / twi), built on the
+// device once per (device, p, K, KC) and kept: 16 B per transform position
+// (128 MiB at L = 2^23).  Used up to L = 2^MC_TWIST_TABLE_MAX_K (default 24);
+// MC_NO_TWIST_TABLE=1 forms the twists on the fly instead (A/B).
+__global__ void twist_table_kernel(TwistTabs tw, int KR, int KC, u32 p, Shoup scale,
+                                   uint2 *outf, uint2 *outi) {
+    const long long L = 1ll << (KR + KC);
+    for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < L;
+         i += (long long)gridDim.x * blockDim.x) {
+        const u32 r = (u32)(i >> KC), x = (u32)(i & ((1ll << KC) - 1));
+        const u32 e = x * (__brev(r) >> (32 - KR));  // < L <= 2^26
+        const u32 wf = pow_w(tw.lo_f, tw.hi_f, e, p);
+        const u32 wi = mul_shoup(pow_w(tw.lo_i, tw.hi_i, e, p), scale, p);
+        outf[i] = make_uint2(wf, shoup_comp(wf, p, tw.two32_over_p));
+        outi[i] = make_uint2(wi, shoup_comp(wi, p, tw.two32_over_p));
+    }
+}
+
+struct FullTwist {
+    uint2 *f = nullptr, *i = nullptr;
+};
+static std::map<std::tuple<int, u32, int, int>, FullTwist> g_full_tw;
+
+static bool twist_table_on(int K) {
+    static const int max_k = [] {
+        const char *e = getenv("MC_NO_TWIST_TABLE");
+        if (e && *e) return 0;
+        const char *m = getenv("MC_TWIST_TABLE_MAX_K");
+        return m && *m ? atoi(m) : 24;
+    }();
+    return K <= max_k;
+}
+
+static mc_status get_full_twist(const FieldTables *T, const TwistTabs &tw, int KC,
+                                const uint2 **f, const uint2 **i) {
+    const int K = T->log2L, KR = K - KC;
+    const int dev = current_device();
+    auto key = std::make_tuple(dev, T->p, K, KC);
+    std::lock_guard<std::mutex> lock(g_tw_mu);
+    auto it = g_full_tw.find(key);
+    if (it == g_full_tw.end()) {
+        FullTwist h;
+        const size_t bytes = sizeof(uint2) << K;
+        cudaError_t e = cudaMalloc(&h.f, bytes);
+        if (e == cudaSuccess) e = cudaMalloc(&h.i, bytes);
+        if (e != cudaSuccess) {
+            cudaFree(h.f);
+            cudaGetLastError();
+            return cuda_fail(e, "twist table allocation");
+        }
+        // L^-1 * 2^32 (the Montgomery pointwise product leaves a 2^-32)
+        const Shoup scale = T->linv_mont;
+        // built on a private stream and finished before the tables are
+        // published: later calls on any stream may use them at once
+        cudaStream_t bs = nullptr;
+        e = cudaStreamCreateWithFlags(&bs, cudaStreamNonBlocking);
+        if (e == cudaSuccess) {
+            twist_table_kernel<<<4 * sm_count(), 256, 0, bs>>>(tw, KR, KC, T->p, scale, h.f, h.i);
+            note_launches(1);
+            e = cudaGetLastError();
+            if (e == cudaSuccess) e = cudaStreamSynchronize(bs);
+            cudaStreamDestroy(bs);
+        }
+        if (e != cudaSuccess) return cuda_fail(e, "twist table build");
+        it = g_full_tw.emplace(key, h).first;
+    }
+    *f = it->second.f;
+    *i = it->second.i;
+    return MC_OK;
+}
+
 mc_status get_twist_tables(u32 p, int K, const u32 **lo_f, const uint2 **hi_f, const u32 **lo_i,
                            const uint2 **hi_i) {
     const FieldTables *T;
@@ -171,23 +281,27 @@ mc_status get_twist_tables(u32 p, int K, const u32 **lo_f, const uint2 **hi_f, c
     return MC_OK;
 }
 
-template <int KC, int AR>
+template <int KC, int AR, bool TT>
 static cudaError_t launch_rows_lz(const FourParams &P, int KR, cudaStream_t st) {
     using RC = RowCfg<KC>;
     static int per_sm = 0;
     if (!per_sm) {
-        cudaError_t e = prep_kernel(row_conv_kernel<KC, AR>, RC::SMEM, RC::THREADS, &per_sm);
+        cudaError_t e = prep_kernel(row_conv_kernel<KC, AR, TT>, RC::SMEM, RC::THREADS, &per_sm);
         if (e != cudaSuccess) return e;
     }
     long long work = (P.nrows * P.chunk + RC::PPC - 1) / RC::PPC;
     long long grid = std::min<long long>(work, (long long)per_sm * sm_count());
-    row_conv_kernel<KC, AR><<<(unsigned)grid, RC::THREADS, RC::SMEM, st>>>(P, KR);
+    row_conv_kernel<KC, AR, TT><<<(unsigned)grid, RC::THREADS, RC::SMEM, st>>>(P, KR);
     return cudaGetLastError();
 }
 
 template <int KC>
 static cudaError_t launch_rows(const FourParams &P, int KR, cudaStream_t st) {
-    return P.cs.ar == 1 ? launch_rows_lz<KC, 1>(P, KR, st) : launch_rows_lz<KC, 2>(P, KR, st);
+    if (P.twf)
+        return P.cs.ar == 1 ? launch_rows_lz<KC, 1, true>(P, KR, st)
+                            : launch_rows_lz<KC, 2, true>(P, KR, st);
+    return P.cs.ar == 1 ? launch_rows_lz<KC, 1, false>(P, KR, st)
+                        : launch_rows_lz<KC, 2, false>(P, KR, st);
 }
 
 static cudaError_t launch_cols_any(int KC, int KR, int NT, const FourParams &P, bool fwd,
@@ -289,6 +403,8 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     FourParams P;
     memset(&P, 0, sizeof(P));
     if ((s = get_twist(TL, &P.tw)) != MC_OK) return s;
+    if (twist_table_on(K) && (s = get_full_twist(TL, P.tw, KC, &P.twf, &P.twi)) != MC_OK)
+        return s;
     P.cs.p = p;
     memcpy(P.cs.mlev, TR->mlev, sizeof(P.cs.mlev));  // column-level ITFT constants
     memcpy(P.cs.hinv, TR->hinv, sizeof(P.cs.hinv));

@@ -36,6 +36,9 @@ struct FourParams {
     const uint2 *col_tf, *col_ti;  // stage tables for the R-point column transforms
     const uint2 *row_tf, *row_ti;  // stage tables for the C-point row transforms
     long long nrows;  // rows of each product the row pass transforms (NT * R/16)
+    // twist tables [R][C] (row_conv_kernel<.., TT = true>): twf[r][x] =
+    // w_L^(x * rev(r)), twi[r][x] = w_L^-(x * rev(r)) * L^-1 * 2^32, Shoup pairs
+    const uint2 *twf, *twi;
 };
 
 __device__ __forceinline__ u32 pow_w(const u32 *lo, const uint2 *hi, u32 e, u32 p) {
