@@ -57,11 +57,11 @@ def test_sweep_64x64_vs_oracle(orc, engine, p):
 
 
 @pytest.mark.parametrize("p", [257, P2])
-def test_sweep_128x128_sampled(orc, p):
-    """Engine sweep over (1..128)^2 (reference tests/test_acceptance.py:85-108),
-    every 3rd z2 to bound runtime; both engines."""
+def test_sweep_128x128(orc, p):
+    """Engine sweep over every (z1, z2) in (1..128)^2 (reference
+    tests/test_acceptance.py:85-108); both engines."""
     for z1 in range(1, 129):
-        for z2 in range(1 + z1 % 3, 129, 3):
+        for z2 in range(1, 129):
             n = z1 + z2 - 1
             if (n - 1).bit_length() > orc.two_adicity(p):
                 continue

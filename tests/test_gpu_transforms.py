@@ -68,9 +68,9 @@ def test_tft_lattice_vs_oracle(orc):
 
 @pytest.mark.parametrize("p", [P1, P3])
 def test_itft_tft_roundtrip_all_n(orc, p):
-    """itft(tft(x)) == L*x for every 1 <= n <= L <= 256
-    (reference tests/test_acceptance.py:62-82 up to 1024 on the CPU)."""
-    for lg in range(0, 9):
+    """itft(tft(x)) == L*x for every 1 <= n <= L <= 1024, the reference's
+    own range (tests/test_acceptance.py:62-82)."""
+    for lg in range(0, 11):
         L = 1 << lg
         for n in range(1, L + 1):
             x = orc.gen_u32(61, 0, L * 1000 + n, 2, n, p)
