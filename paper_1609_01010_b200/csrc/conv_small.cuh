@@ -35,6 +35,8 @@
 // output equals the reference's bit for bit; see tests/kernel_model.py for
 // the position-level model checked against the oracle.
 #pragma once
+#include <type_traits>
+
 #include "modarith.cuh"
 #include "tma.cuh"
 
@@ -71,10 +73,20 @@ struct ConvSmallParams {
     int ready_rows;         // products per chunk
 };
 
-// 32-bank conflict-free swizzle for the three access patterns used here:
-// lanes -> position bits [0,5), [4,9), or [0,4) + {8}.  XOR touches only the
-// low 5 bits, so it is a permutation of every aligned 32-word row.
-__device__ __forceinline__ int swz(int x) { return x ^ (((x >> 5) & 15) | ((x >> 4) & 16)); }
+// Shared-memory swizzle of the exchanges: XOR of position bits [2,5) with
+// bits 4-6 and 8, a permutation of every aligned 32-word row that keeps each
+// aligned quad of positions together (bits 0-1 untouched).  Conflict-free
+// for every exchange pattern of the register passes: scalar accesses with
+// lanes -> position bits [0,5) (top-pass and SB = 8 layouts) or [0,4) + {8}
+// (SB = 4), and 16-byte vector accesses in the SB = 0 layout, where a thread
+// holds 16 consecutive positions (four LDS.128 / STS.128 instead of 16
+// scalar ones; every quarter-warp hits 8 distinct 16-byte bank groups).
+__device__ __forceinline__ int swz(int x) { return x ^ ((((x >> 4) & 7) << 2) ^ ((x >> 4) & 16)); }
+
+// Scalar-only swizzle (XOR of bits [0,5) with bits 5-8): conflict-free for
+// lanes -> bits [0,5), [4,9), [0,4) + {8} with scalar accesses, and for the
+// bit-reversal permutations of the standalone transforms (xform_small.cuh).
+__device__ __forceinline__ int swz_xf(int x) { return x ^ (((x >> 5) & 15) | ((x >> 4) & 16)); }
 
 template <int SB>
 __device__ __forceinline__ int slot_pos(int t, int s) {
@@ -225,11 +237,13 @@ __device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallPa
 
 // ---------------------------------------------------------------- top pass (inverse)
 // transform.py:451-489 restricted to slot granularity.  M, N, OFF in slots;
-// level index LV = log2 M (m = M*G elements).  Lazy modes (AR != 0) only for
-// the complete transform (N == M), which is a plain DIT.
+// level index LV = log2 M (m = M*G elements).  In a lazy mode (AR != 0) the
+// complete sub-transforms and the closing DIT butterflies run lazily; the
+// truncation steps (pre-adds, cross butterflies, combines), whose modular
+// sums need canonical operands, canonicalise exactly those operands first
+// (Shoup products accept any word).  Outputs are in the mode's inverse range.
 template <int K, int M, int N, int OFF, int AR = 0>
 struct ItftTop {
-    static_assert(AR == 0 || N == M || N == 0, "lazy ranges only on the complete inverse");
     static __device__ __forceinline__ void run(u32 (&v)[16], int t, const ConvSmallParams &P,
                                                const Tw &W) {
         constexpr int G = 1 << (K - 4);
@@ -241,13 +255,14 @@ struct ItftTop {
         } else if constexpr (N <= H) {
             // pre: time values of both halves folded into the first half
 #pragma unroll
-            for (int s = N; s < H; ++s) v[OFF + s] = add_mod(v[OFF + s], v[OFF + s + H], p);
-            ItftTop<K, H, N, OFF>::run(v, t, P, W);
+            for (int s = N; s < H; ++s)
+                v[OFF + s] = add_mod(canon_t<AR>(v[OFF + s], p), canon_t<AR>(v[OFF + s + H], p), p);
+            ItftTop<K, H, N, OFF, AR>::run(v, t, P, W);
             // combine: m*u_i = 2*(h*(u_i + u_{i+h})) - m*u_{i+h}
             const Shoup mm = P.mlev[LV];
 #pragma unroll
             for (int s = 0; s < N; ++s) {
-                u32 a = v[OFF + s];
+                const u32 a = canon_t<AR>(v[OFF + s], p);
                 v[OFF + s] = sub_mod(add_mod(a, a, p), mul_shoup(v[OFF + s + H], mm, p), p);
             }
         } else {
@@ -257,7 +272,7 @@ struct ItftTop {
             constexpr int h = H * G;
 #pragma unroll
             for (int s = N - H; s < H; ++s) {  // cross butterflies
-                u32 a = v[OFF + s], b = v[OFF + s + H];
+                const u32 a = canon_t<AR>(v[OFF + s], p), b = canon_t<AR>(v[OFF + s + H], p);
                 const uint2 w = ldtw(W.tf, h + t + G * s);
                 u32 d = sub_mod(mul_shoup(a, ih, p), add_mod(b, b, p), p);
                 v[OFF + s + H] = mul_shoup(d, w.x, w.y, p);
@@ -273,18 +288,12 @@ struct ItftTop {
     }
 };
 
-// Inverse top pass in mode AR; the truncated recursion (NT < 16) runs on
-// canonical residues, so lazy values are canonicalised first.
+// Inverse top pass (complete or truncated) in mode AR; outputs in the mode's
+// inverse range (canon_t before storing).
 template <int K, int NT, int AR>
 __device__ __forceinline__ void inv_top(u32 (&v)[16], int t, const ConvSmallParams &P,
                                         const Tw &W) {
-    if constexpr (NT < 16 && AR != 0) {
-#pragma unroll
-        for (int s = 0; s < 16; ++s) v[s] = canon_t<AR>(v[s], P.p);
-        ItftTop<K, 16, NT, 0, 0>::run(v, t, P, W);
-    } else {
-        ItftTop<K, 16, NT, 0, AR>::run(v, t, P, W);
-    }
+    ItftTop<K, 16, NT, 0, AR>::run(v, t, P, W);
 }
 
 // ---------------------------------------------------------------- exchange
@@ -296,6 +305,10 @@ struct LaySmall {
     __device__ __forceinline__ int operator()(int x) const { return swz(x); }
 };
 
+struct LayXf {  // standalone transforms: scalar accesses only (swz_xf)
+    __device__ __forceinline__ int operator()(int x) const { return swz_xf(x); }
+};
+
 template <int TC>
 struct LayCol {
     int c;
@@ -305,14 +318,32 @@ struct LayCol {
 
 template <int SB, class Lay = LaySmall>
 __device__ __forceinline__ void put(u32 *buf, const u32 (&v)[16], int t, Lay lay = Lay()) {
+    if constexpr (SB == 0 && std::is_same<Lay, LaySmall>::value) {
 #pragma unroll
-    for (int s = 0; s < 16; ++s) buf[lay(slot_pos<SB>(t, s))] = v[s];
+        for (int k = 0; k < 4; ++k)  // positions 16t + 4k .. +3: one aligned quad
+            *reinterpret_cast<uint4 *>(buf + swz(16 * t + 4 * k)) =
+                make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+    } else {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) buf[lay(slot_pos<SB>(t, s))] = v[s];
+    }
 }
 
 template <int SB, class Lay = LaySmall>
 __device__ __forceinline__ void get(const u32 *buf, u32 (&v)[16], int t, Lay lay = Lay()) {
+    if constexpr (SB == 0 && std::is_same<Lay, LaySmall>::value) {
 #pragma unroll
-    for (int s = 0; s < 16; ++s) v[s] = buf[lay(slot_pos<SB>(t, s))];
+        for (int k = 0; k < 4; ++k) {
+            const uint4 q = *reinterpret_cast<const uint4 *>(buf + swz(16 * t + 4 * k));
+            v[4 * k] = q.x;
+            v[4 * k + 1] = q.y;
+            v[4 * k + 2] = q.z;
+            v[4 * k + 3] = q.w;
+        }
+    } else {
+#pragma unroll
+        for (int s = 0; s < 16; ++s) v[s] = buf[lay(slot_pos<SB>(t, s))];
+    }
 }
 
 // Lower-pass plan for K: up to three passes (bits [8,KL), [4,8), [0,4) with
@@ -600,7 +631,7 @@ conv_small_kernel(const ConvSmallParams P) {
             __syncthreads();  // every thread is done reading bufA
 #pragma unroll
             for (int s = 0; s < 16; ++s)
-                stg[(s << (K - 4)) | t] = canon_t<(NT < 16 ? 0 : AR)>(va[s], P.p);
+                stg[(s << (K - 4)) | t] = canon_t<AR>(va[s], P.p);
             fence_proxy_async_smem();
             __syncthreads();
             const int head = min((4 - mis) & 3, P.n);
@@ -616,7 +647,7 @@ conv_small_kernel(const ConvSmallParams P) {
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 const int x = (s << (K - 4)) | t;
-                if (x < P.n) __stcs(gc + x, canon_t<(NT < 16 ? 0 : AR)>(va[s], P.p));
+                if (x < P.n) __stcs(gc + x, canon_t<AR>(va[s], P.p));
             }
         }
     }

@@ -68,12 +68,12 @@ __device__ __forceinline__ void store_col(u32 *dst, const u32 (&v)[16], int t, l
     u32 *base = dst + (long long)t * Ccols + col;
     if (15 * SLOT + (long long)(C::G - 1) * Ccols + tile_col0 + C::TC - 1 < P.n) {
 #pragma unroll
-        for (int s = 0; s < 16; ++s) __stcs(base + s * SLOT, canon_t<(NT < 16 ? 0 : AR)>(v[s], P.cs.p));
+        for (int s = 0; s < 16; ++s) __stcs(base + s * SLOT, canon_t<AR>(v[s], P.cs.p));
     } else {
         const long long idx0 = (long long)t * Ccols + col;
 #pragma unroll
         for (int s = 0; s < 16; ++s)
-            if (idx0 + s * SLOT < P.n) __stcs(base + s * SLOT, canon_t<(NT < 16 ? 0 : AR)>(v[s], P.cs.p));
+            if (idx0 + s * SLOT < P.n) __stcs(base + s * SLOT, canon_t<AR>(v[s], P.cs.p));
     }
 }
 

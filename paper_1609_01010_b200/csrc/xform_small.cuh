@@ -66,12 +66,12 @@ xform_small_kernel(const XformParams X) {
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 const int k = t + G * s;
-                buf[swz(brev_k<K>(k))] = valid ? mul_shoup(__ldcs(gx + k), 1u, X.red_wp, p) : 0u;
+                buf[swz_xf(brev_k<K>(k))] = valid ? mul_shoup(__ldcs(gx + k), 1u, X.red_wp, p) : 0u;
             }
             __syncthreads();
 #pragma unroll
-            for (int s = 0; s < 16; ++s) v[s] = buf[swz(slot_pos<SBL>(t, s))];
-            inv_lower_chain1<K, Plan<K>::NP - 1, LaySmall, 16>(buf, v, t, X.cs, W, LaySmall());
+            for (int s = 0; s < 16; ++s) v[s] = buf[swz_xf(slot_pos<SBL>(t, s))];
+            inv_lower_chain1<K, Plan<K>::NP - 1, LayXf, 16>(buf, v, t, X.cs, W, LayXf());
             ItftTop<K, 16, 16, 0>::run(v, t, X.cs, W);
             if (valid) {
 #pragma unroll
@@ -84,21 +84,21 @@ xform_small_kernel(const XformParams X) {
                 v[s] = (valid && x < X.z) ? mul_shoup(__ldcs(gx + x), 1u, X.red_wp, p) : 0u;
             }
             fwd_top<K, NT>(v, X.z, t, X.cs, W);
-            fwd_lower_chain1<K, 0, LaySmall, NT>(buf, v, t, X.cs, W, LaySmall());
+            fwd_lower_chain1<K, 0, LayXf, NT>(buf, v, t, X.cs, W, LayXf());
             // v[s] = X[rev(x)] at x = slot_pos<SBL>(t, s); stage it for a coalesced store
             __syncthreads();
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 const int x = slot_pos<SBL>(t, s);
                 if (NT >= 16 || (x >> (K - 4)) < NT)
-                    buf[swz(MODE == MODE_NTT_FWD ? brev_k<K>(x) : x)] = v[s];
+                    buf[swz_xf(MODE == MODE_NTT_FWD ? brev_k<K>(x) : x)] = v[s];
             }
             __syncthreads();
             if (valid) {
 #pragma unroll
                 for (int s = 0; s < 16; ++s) {
                     const int x = t + G * s;
-                    if (MODE == MODE_NTT_FWD || x < X.n) __stcs(gy + x, buf[swz(x)]);
+                    if (MODE == MODE_NTT_FWD || x < X.n) __stcs(gy + x, buf[swz_xf(x)]);
                 }
             }
         }
