@@ -4,13 +4,18 @@
 //   mc_tft   transform.py:379-448  first n bit-reversed spectral values
 //   mc_itft  transform.py:451-529  L * u_i, i < n, from n spectral values
 //
-// Level-scheduled on global memory: one launch per butterfly level over
-// all rows of the batch (any L up to 2^27, limited by the field).  Twiddles
+// Three tiers: the fused register-pass kernels (xform_small.cuh) for moddft
+// and tft with n > L/2 at 16 <= L <= 8192; row-resident shared-memory
+// kernels (rows_kernel) for the exact truncated transforms (itft, tft with
+// n <= L/2) at L <= 2^14; otherwise level-scheduled on global memory: one
+// launch per butterfly level over all rows of the batch (any L up to 2^27,
+// limited by the field).  Twiddles
 // w_{2h}^j = w_L^(j*L/2h) come from the two-level power tables of the
 // four-step path (lo[e & 4095] * hi[e >> 12]); the variable-twiddle
 // products use Montgomery multiplication with the twiddle in Montgomery
 // form.  These entry points exist for call-compatibility of
 // moddft/tft/itft; the convolution hot path never uses them.
+#include <algorithm>
 #include <vector>
 
 #include "fourstep.cuh"
@@ -269,6 +274,192 @@ mc_status levels_conv(const u32 *a, long long lda, int z1, const u32 *b, long lo
     return MC_OK;
 }
 
+// ---------------------------------------------------------------- row-resident (L <= 2^14)
+// Exact truncated transforms with one CTA per row and the row resident in
+// shared memory: every level of the reference recursion is one pass over
+// the row between two barriers, twiddles are the Shoup stage tables
+// (tf/ti, L2-resident).  Serves itft (every n) and tft with n <= L/2 (the
+// fused register passes take n > L/2), replacing one launch per level on
+// global memory.
+constexpr int kRowsMaxK = 14;
+constexpr int kChainMax = 16;
+
+struct RowsParams {
+    const u32 *x;
+    long long ldx;
+    u32 *y;
+    long long ldy;
+    long long batch;
+    int K, z, n;
+    u32 p, red_wp;
+    const uint2 *tf;  // tf[h + j] = w_{2h}^j (Shoup pairs)
+    const uint2 *ti;  // ti[h + j] = w_{2h}^-j
+    // itft: the partial path of the van der Hoeven recursion, top-down
+    int nc;
+    int c_off[kChainMax], c_h[kChainMax], c_n[kChainMax];
+    Shoup c_mm[kChainMax], c_ih[kChainMax];  // m mod p, h^-1 mod p of each node
+};
+
+__device__ __forceinline__ u32 mul_tw(u32 x, uint2 w, u32 p) { return mul_shoup(x, w.x, w.y, p); }
+
+// MODE 0: tft (transform.py:379-418, levels top-down, pruned by z and n);
+// MODE 1: itft (transform.py:451-489): the complete sub-blocks of the
+// recursion are the aligned 2h-chunks inside [0, n) (the blocks are the
+// binary decomposition of n), run as inverse DIT stages bottom-up; then the
+// partial path top-down (cross / pre-add) and bottom-up (DIT / combine).
+template <int MODE>
+__global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
+    extern __shared__ uint4 smem_rows[];
+    u32 *s = reinterpret_cast<u32 *>(smem_rows);
+    const int L = 1 << P.K, n = P.n, NTH = blockDim.x, tid = threadIdx.x;
+    const u32 p = P.p;
+    for (long long r = blockIdx.x; r < P.batch; r += gridDim.x) {
+        const u32 *xr = P.x + r * P.ldx;
+        const int zin = MODE == 0 ? P.z : n;
+        __syncthreads();  // the previous row's stores have read s
+        for (int i = tid; i < L; i += NTH) s[i] = i < zin ? mul_shoup(__ldcs(xr + i), 1u, P.red_wp, p) : 0u;
+        __syncthreads();
+        if (MODE == 0) {
+            for (int h = L >> 1; h >= 1; h >>= 1) {
+                const int m = 2 * h;
+                const int nblk = (n + m - 1) / m;
+                const int zz = P.z < m ? P.z : m;
+                const int per = nblk * h;
+                for (int k = tid; k < per; k += NTH) {
+                    const int j = k & (h - 1);
+                    if (j >= zz) continue;
+                    const int lo = (k / h) * m + j, hi = lo + h;
+                    const bool b_zero = j + h >= zz;
+                    if (lo - j + h < n) {  // hi output needed
+                        const uint2 w = __ldg(P.tf + h + j);
+                        if (b_zero) {
+                            s[hi] = mul_tw(s[lo], w, p);
+                        } else {
+                            const u32 a = s[lo], c = s[hi];
+                            s[lo] = add_mod(a, c, p);
+                            s[hi] = mul_tw(sub_mod(a, c, p), w, p);
+                        }
+                    } else if (!b_zero) {
+                        s[lo] = add_mod(s[lo], s[hi], p);
+                    }
+                }
+                __syncthreads();
+            }
+        } else {
+            // 1. complete blocks: inverse DIT, stage h over the aligned 2h-chunks below n
+            for (int h = 1; h < L; h <<= 1) {
+                const int per = (n / (2 * h)) * h;
+                if (per == 0) break;
+                for (int k = tid; k < per; k += NTH) {
+                    const int j = k & (h - 1);
+                    const int lo = (k / h) * 2 * h + j, hi = lo + h;
+                    const u32 t = mul_tw(s[hi], __ldg(P.ti + h + j), p);
+                    const u32 a = s[lo];
+                    s[lo] = add_mod(a, t, p);
+                    s[hi] = sub_mod(a, t, p);
+                }
+                __syncthreads();
+            }
+            // 2. down the partial path: cross butterflies (n > h) or pre-adds
+            for (int c = 0; c < P.nc; ++c) {
+                const int off = P.c_off[c], h = P.c_h[c], nn = P.c_n[c];
+                u32 *row = s + off;
+                if (nn > h) {
+                    const Shoup mm = P.c_mm[c], ih = P.c_ih[c];
+                    for (int i = nn - h + tid; i < h; i += NTH) {
+                        const u32 a = row[i], b = row[i + h];
+                        const u32 d = sub_mod(mul_shoup(a, ih, p), add_mod(b, b, p), p);
+                        row[i + h] = mul_tw(d, __ldg(P.tf + h + i), p);
+                        row[i] = sub_mod(add_mod(a, a, p), mul_shoup(b, mm, p), p);
+                    }
+                } else {
+                    for (int i = nn + tid; i < h; i += NTH) row[i] = add_mod(row[i], row[i + h], p);
+                }
+                __syncthreads();
+            }
+            // 3. up the partial path: DIT butterflies (n > h) or combines
+            for (int c = P.nc - 1; c >= 0; --c) {
+                const int off = P.c_off[c], h = P.c_h[c], nn = P.c_n[c];
+                u32 *row = s + off;
+                if (nn > h) {
+                    for (int i = tid; i < nn - h; i += NTH) {
+                        const u32 t = mul_tw(row[i + h], __ldg(P.ti + h + i), p);
+                        const u32 a = row[i];
+                        row[i] = add_mod(a, t, p);
+                        row[i + h] = sub_mod(a, t, p);
+                    }
+                } else {
+                    const Shoup mm = P.c_mm[c];
+                    for (int i = tid; i < nn; i += NTH) {
+                        const u32 a = row[i];
+                        row[i] = sub_mod(add_mod(a, a, p), mul_shoup(row[i + h], mm, p), p);
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        u32 *yr = P.y + r * P.ldy;
+        for (int i = tid; i < n; i += NTH) __stcs(yr + i, s[i]);
+    }
+}
+
+static mc_status rows_launch(int mode, const u32 *x, long long ldx, int z, u32 *y, long long ldy,
+                             int n, int K, long long batch, u32 p, cudaStream_t st) {
+    const FieldTables *T;
+    mc_status s = get_tables(p, K, &T);
+    if (s != MC_OK) return s;
+    RowsParams R;
+    memset(&R, 0, sizeof(R));
+    R.x = x;
+    R.ldx = ldx;
+    R.y = y;
+    R.ldy = ldy;
+    R.batch = batch;
+    R.K = K;
+    R.z = z;
+    R.n = n;
+    R.p = p;
+    R.red_wp = (u32)((1ull << 32) / p);
+    R.tf = T->tf;
+    R.ti = T->ti;
+    if (mode == 1) {  // partial path of _itft_recurse (transform.py:451-489)
+        long long off = 0, m = 1ll << K, nn = n;
+        while (m > 1 && nn > 0 && nn < m) {
+            const long long h = m >> 1;
+            if (R.nc >= kChainMax) return fail(MC_EINVAL, "itft chain too long");
+            R.c_off[R.nc] = (int)off;
+            R.c_h[R.nc] = (int)h;
+            R.c_n[R.nc] = (int)nn;
+            R.c_mm[R.nc] = shoup((u32)(m % p), p);
+            R.c_ih[R.nc] = shoup(inv_mod((u32)(h % p), p), p);
+            ++R.nc;
+            if (nn > h) {
+                off += h;
+                nn -= h;
+            }
+            m = h;
+        }
+    }
+    const int L = 1 << K;
+    const int threads = std::max(32, std::min(512, L / 8));
+    const size_t smem = 4ull * L;
+    static const int max_dyn = [] {
+        cudaFuncSetAttribute(rows_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kRowsMaxK);
+        cudaFuncSetAttribute(rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kRowsMaxK);
+        return 4 << kRowsMaxK;
+    }();
+    (void)max_dyn;
+    const int per_sm = std::max(1, std::min(2048 / threads, (int)((200u << 10) / smem)));
+    const long long grid = std::min<long long>(batch, (long long)sm_count() * per_sm);
+    if (mode == 0)
+        rows_kernel<0><<<(unsigned)grid, threads, smem, st>>>(R);
+    else
+        rows_kernel<1><<<(unsigned)grid, threads, smem, st>>>(R);
+    note_launches(1);
+    MC_CUDA_CHECK(cudaGetLastError());
+    return MC_OK;
+}
+
 // ---------------------------------------------------------------- fused (L <= 8192)
 // MC_XFORM_LEVELS (non-empty) forces the level-scheduled kernels (A/B, parity).
 static bool xform_levels_forced() {
@@ -388,6 +579,8 @@ mc_status mc_tft(const uint32_t *x, int32_t z, uint32_t *y, int32_t n, int32_t l
     cudaStream_t st = (cudaStream_t)stream;
     if (log2L >= 4 && log2L <= kSmallMaxK && 2ll * n > L && !xform_levels_forced())
         return xform_small(MODE_TFT, x, z, z, y, n, n, log2L, batch, p, st);
+    if (log2L <= kRowsMaxK && !xform_levels_forced())
+        return rows_launch(0, x, z, z, y, n, n, log2L, batch, p, st);
     u32 *w = nullptr;
     keep_pool_memory();
     MC_CUDA_CHECK(cudaMallocAsync(&w, 4ull * L * batch, st));
@@ -423,6 +616,8 @@ mc_status mc_itft(const uint32_t *xhat, uint32_t *y, int32_t n, int32_t log2L, i
     if (s != MC_OK || batch == 0) return s;
     if (!xhat || !y) return fail(MC_EINVAL, "null pointer");
     cudaStream_t st = (cudaStream_t)stream;
+    if (log2L <= kRowsMaxK && !xform_levels_forced())
+        return rows_launch(1, xhat, n, n, y, n, n, log2L, batch, p, st);
     u32 *w = nullptr;
     keep_pool_memory();
     MC_CUDA_CHECK(cudaMallocAsync(&w, 4ull * L * batch, st));

@@ -150,3 +150,30 @@ def test_usage_errors():
         mc.itft(t, [1] * 9)
     with pytest.raises(ValueError):
         mc.itft(t, [])
+
+
+@pytest.mark.parametrize("lg", [5, 11, 12, 13, 14])
+@pytest.mark.parametrize("p", [P1, P3])
+def test_row_resident_truncated_vs_oracle(orc, lg, p):
+    """The row-resident kernels (itft at every n, tft with n <= L/2; L <=
+    2^14), batched, against the oracle at the truncation boundaries, with an
+    all-(p-1) row."""
+    L = 1 << lg
+    B = 3
+    sh = _tensors.stream_handle()
+    for n in sorted({1, 2, L // 2 - 1, L // 2, L // 2 + 1, L - L // 5, L - 1, L}):
+        x = orc.gen_u32(64, 0, lg * 100000 + n, B, n, p)
+        x[1, :] = p - 1
+        xt = torch.from_numpy(x.view(np.int32)).cuda()
+        y = torch.empty((B, n), dtype=torch.int32, device="cuda")
+        _native.check(_native.lib().mc_itft(xt.data_ptr(), y.data_ptr(), n, lg, B, p, sh))
+        got = y.cpu().numpy().view(np.uint32)
+        for r in range(B):
+            assert np.array_equal(got[r], orc.itft(x[r], L, p)[0]), ("itft", L, n, r)
+        for z in sorted({1, n // 3 + 1, n}):
+            xz = torch.from_numpy(np.ascontiguousarray(x[:, :z]).view(np.int32)).cuda()
+            t = torch.empty((B, n), dtype=torch.int32, device="cuda")
+            _native.check(_native.lib().mc_tft(xz.data_ptr(), z, t.data_ptr(), n, lg, B, p, sh))
+            got = t.cpu().numpy().view(np.uint32)
+            for r in range(B):
+                assert np.array_equal(got[r], orc.tft(x[r, :z], n, L, p)[0]), ("tft", L, n, z, r)
