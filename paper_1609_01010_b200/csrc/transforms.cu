@@ -302,6 +302,17 @@ struct RowsParams {
 
 __device__ __forceinline__ u32 mul_tw(u32 x, uint2 w, u32 p) { return mul_shoup(x, w.x, w.y, p); }
 
+// Row in shared memory, one pad word per 16 (position x at x + x/16): the
+// stride-16 accesses of the register passes hit 32 distinct banks.
+struct PadRow {
+    u32 *s;
+    int off;
+    __device__ __forceinline__ u32 &operator[](int x) const {
+        const int y = off + x;
+        return s[y + (y >> 4)];
+    }
+};
+
 // MODE 0: tft (transform.py:379-418, levels top-down, pruned by z and n);
 // MODE 1: itft (transform.py:451-489): the complete sub-blocks of the
 // recursion are the aligned 2h-chunks inside [0, n) (the blocks are the
@@ -310,7 +321,7 @@ __device__ __forceinline__ u32 mul_tw(u32 x, uint2 w, u32 p) { return mul_shoup(
 template <int MODE>
 __global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
     extern __shared__ uint4 smem_rows[];
-    u32 *s = reinterpret_cast<u32 *>(smem_rows);
+    const PadRow s{reinterpret_cast<u32 *>(smem_rows), 0};
     const int L = 1 << P.K, n = P.n, NTH = blockDim.x, tid = threadIdx.x;
     const u32 p = P.p;
     for (long long r = blockIdx.x; r < P.batch; r += gridDim.x) {
@@ -346,8 +357,59 @@ __global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
                 __syncthreads();
             }
         } else {
-            // 1. complete blocks: inverse DIT, stage h over the aligned 2h-chunks below n
-            for (int h = 1; h < L; h <<= 1) {
+            // 1. complete blocks: inverse DIT, stage h over the aligned 2h-chunks
+            // below n.  Four stages at a time (h = S .. 8S, S = 16^q) run in
+            // registers on the aligned 16S-chunks below n (16 elements at
+            // stride S per thread); the tail [16S * floor(n / 16S), n) runs
+            // those stages one at a time.  Leftover top stages (K mod 4) and
+            // all stages with no complete 16S-chunk run one at a time.
+            int h = 1;
+            for (int S = 1; 16 * S <= L; S *= 16) {
+                const int CH = 16 * S, full = n / CH;
+                if (full == 0) break;
+                const int lgS = __ffs(S) - 1;
+                for (int k = tid; k < full * S; k += NTH) {
+                    const PadRow base{s.s, (k >> lgS) * CH + (k & (S - 1))};
+                    const int o = k & (S - 1);
+                    u32 v[16];
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) v[q] = base[q * S];
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const int hh = S << b;
+#pragma unroll
+                        for (int q = 0; q < 16; ++q) {
+                            if (q & (1 << b)) continue;
+                            const int j = (q & ((1 << b) - 1)) * S + o;
+                            const u32 t = mul_tw(v[q + (1 << b)], __ldg(P.ti + hh + j), p);
+                            const u32 a = v[q];
+                            v[q] = add_mod(a, t, p);
+                            v[q + (1 << b)] = sub_mod(a, t, p);
+                        }
+                    }
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) base[q * S] = v[q];
+                }
+                // tail stages (disjoint from the chunks above)
+                for (int b = 0; b < 4; ++b) {
+                    const int hh = S << b;
+                    const int k0 = full * CH / 2, per = (n / (2 * hh)) * hh;
+                    if (per > k0) {
+                        for (int k = k0 + tid; k < per; k += NTH) {
+                            const int j = k & (hh - 1);
+                            const int lo = (k / hh) * 2 * hh + j, hi = lo + hh;
+                            const u32 t = mul_tw(s[hi], __ldg(P.ti + hh + j), p);
+                            const u32 a = s[lo];
+                            s[lo] = add_mod(a, t, p);
+                            s[hi] = sub_mod(a, t, p);
+                        }
+                        __syncthreads();
+                    }
+                }
+                __syncthreads();
+                h = 16 * S;
+            }
+            for (; h < L; h <<= 1) {
                 const int per = (n / (2 * h)) * h;
                 if (per == 0) break;
                 for (int k = tid; k < per; k += NTH) {
@@ -363,7 +425,7 @@ __global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
             // 2. down the partial path: cross butterflies (n > h) or pre-adds
             for (int c = 0; c < P.nc; ++c) {
                 const int off = P.c_off[c], h = P.c_h[c], nn = P.c_n[c];
-                u32 *row = s + off;
+                const PadRow row{s.s, off};
                 if (nn > h) {
                     const Shoup mm = P.c_mm[c], ih = P.c_ih[c];
                     for (int i = nn - h + tid; i < h; i += NTH) {
@@ -380,7 +442,7 @@ __global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
             // 3. up the partial path: DIT butterflies (n > h) or combines
             for (int c = P.nc - 1; c >= 0; --c) {
                 const int off = P.c_off[c], h = P.c_h[c], nn = P.c_n[c];
-                u32 *row = s + off;
+                const PadRow row{s.s, off};
                 if (nn > h) {
                     for (int i = tid; i < nn - h; i += NTH) {
                         const u32 t = mul_tw(row[i + h], __ldg(P.ti + h + i), p);
@@ -441,12 +503,12 @@ static mc_status rows_launch(int mode, const u32 *x, long long ldx, int z, u32 *
         }
     }
     const int L = 1 << K;
-    const int threads = std::max(32, std::min(512, L / 8));
-    const size_t smem = 4ull * L;
+    const int threads = std::max(32, std::min(512, L / 16));
+    const size_t smem = 4ull * (L + L / 16 + 1);
     static const int max_dyn = [] {
-        cudaFuncSetAttribute(rows_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kRowsMaxK);
-        cudaFuncSetAttribute(rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 << kRowsMaxK);
-        return 4 << kRowsMaxK;
+        cudaFuncSetAttribute(rows_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * ((1 << kRowsMaxK) + (1 << (kRowsMaxK - 4)) + 1));
+        cudaFuncSetAttribute(rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * ((1 << kRowsMaxK) + (1 << (kRowsMaxK - 4)) + 1));
+        return 4 * ((1 << kRowsMaxK) + (1 << (kRowsMaxK - 4)) + 1);
     }();
     (void)max_dyn;
     const int per_sm = std::max(1, std::min(2048 / threads, (int)((200u << 10) / smem)));
