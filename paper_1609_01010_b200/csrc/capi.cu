@@ -6,6 +6,7 @@
 #include <cuda.h>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "conv_small.cuh"
 #include "fourstep.cuh"
@@ -245,6 +246,10 @@ struct PipeState {
     uint32_t *flags = nullptr;
     uint32_t epoch = 0;
     cudaEvent_t ev_k = nullptr, ev_cp = nullptr;
+    // copy-engine mode: whole-batch device buffers + per-chunk events
+    void *ce_buf = nullptr;
+    size_t ce_bytes = 0;
+    std::vector<cudaEvent_t> ce_in, ce_cmp;
     // recorded on the caller's stream at the end of every call: the next call's
     // internal streams wait on it, so reused buffers are never overwritten
     // while an earlier call (possibly on another caller stream) still uses them
@@ -274,10 +279,16 @@ static std::mutex g_pipe_mu;
 //   2  zero copy (the kernel reads and writes page-locked host memory):
 //      calls under 8 MiB (latency bound), and one-product-per-CTA sizes
 //      (L >= 2048, bulk-store epilogue) with under 512 MiB of operands;
-//   1  streamed inputs + zero-copy output (stream_in_call): one-product-per-
-//      CTA sizes with >= 512 MiB of operands (large copy-engine chunks);
+//   3  copy engines both ways over whole-batch device buffers (ce_full_call):
+//      one-product-per-CTA sizes with >= 512 MiB of operands, contiguous
+//      rows (config 3: 1.39M products/s; streamed inputs 1.34M);
+//   1  streamed inputs + zero-copy output (stream_in_call): the same sizes
+//      when mode 3 does not apply (strided rows, > 8 GiB of buffers);
 //   0  chunked copy pipeline (other sizes).
-// MC_HOST_MODE=zc|in|pipe forces a mode where the size allows it (tests, A/B).
+// Zero copy stays the default below 512 MiB: at config 2 sizes the
+// copy-engine pipeline measured 2.06-2.36M products/s at 6-24 chunks against
+// 2.61M (every chunk's operands must land before its products can leave).
+// MC_HOST_MODE=zc|ce|in|pipe forces a mode where the size allows it (tests, A/B).
 static int zero_copy_shape(int64_t n, int64_t z12, int64_t batch) {
     int K = 0;
     while ((1ll << K) < n) ++K;
@@ -285,6 +296,7 @@ static int zero_copy_shape(int64_t n, int64_t z12, int64_t batch) {
     const char *m = getenv("MC_HOST_MODE");  // read per call
     if (m && *m) {
         if (!strcmp(m, "zc")) return 2;
+        if (!strcmp(m, "ce")) return 3;
         if (!strcmp(m, "in")) return K >= 11 ? 1 : 0;
         return 0;
     }
@@ -292,7 +304,7 @@ static int zero_copy_shape(int64_t n, int64_t z12, int64_t batch) {
     if (K < 11) return 0;
     const char *e = getenv("MC_STREAM_IN_MIN_MB");  // read per call (tests force the mode)
     const long long min_mb = e && *e ? atoll(e) : 512;
-    return 4 * z12 * batch < (min_mb << 20) ? 2 : 1;
+    return 4 * z12 * batch < (min_mb << 20) ? 2 : 3;
 }
 
 // Host memory the device can address directly (page-locked, mapped into the
@@ -395,6 +407,94 @@ static int stream_in_call(PipeState &S, int engine, const uint32_t *a, int64_t l
     return 0;
 }
 
+// Copy engines both ways, whole-batch device buffers: operand chunks go H2D
+// back to back on one stream, each chunk's fused kernel runs on a second as
+// soon as its rows land, its products go D2H on a third.  No buffer is
+// reused inside a call, so the H2D stream never waits and both copy
+// directions run concurrently (measured at cfg2 sizes: 59 MB each way in
+// 1.20-1.24 ms with up to 8 chunks, ~96 GB/s together, against ~72 GB/s for
+// kernel reads and writes of host memory; scripts/ce_gate_probe.py).
+// Returns 1 (not applicable) to fall back.
+static int ce_full_call(PipeState &S, int engine, const uint32_t *a, int64_t lda, int32_t z1,
+                        const uint32_t *b, int64_t ldb, int32_t z2, uint32_t *c, int64_t ldc,
+                        int64_t batch, uint32_t p, cudaStream_t user, mc_status *out) {
+    const int64_t n = (int64_t)z1 + z2 - 1;
+    if (lda != z1 || ldb != z2 || ldc != n) return 1;  // linear DMA per chunk only
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t sa = up(4ull * batch * z1), sb = up(4ull * batch * z2), sc = up(4ull * batch * n);
+    if (sa + sb + sc > (8ull << 30)) return 1;
+    auto fail_out = [&](mc_status st) { *out = st; return 0; };
+    // chunk plan: equal chunks.  The products of a chunk leave only after its
+    // operands have arrived, so the D2H stream trails the H2D stream by one
+    // chunk: time ~ T (1 + 1/N) + N o, o the per-chunk cost of the copies and
+    // the kernel launch.  32 chunks measured best on config 3 (4.3 GB moved:
+    // 1.39M products/s vs 1.34M streamed inputs, 1.30M at 128 chunks);
+    // MC_CE_CHUNKS overrides.
+    const char *ce_env = getenv("MC_CE_CHUNKS");
+    int64_t nchunk = ce_env && *ce_env ? std::max(1, atoi(ce_env)) : 32;
+    nchunk = std::min<int64_t>(nchunk, batch);
+    std::vector<int64_t> rows;
+    const int64_t per = (batch + nchunk - 1) / nchunk;
+    for (int64_t r = 0; r < batch; r += per) rows.push_back(std::min(per, batch - r));
+    const size_t nch = rows.size();
+    while (S.ce_in.size() < nch) {
+        cudaEvent_t e1, e2;
+        if (cudaEventCreateWithFlags(&e1, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&e2, cudaEventDisableTiming) != cudaSuccess)
+            return fail_out(cuda_fail(cudaGetLastError(), "copy-engine events"));
+        S.ce_in.push_back(e1);
+        S.ce_cmp.push_back(e2);
+    }
+    if (!S.ev_k && cudaEventCreateWithFlags(&S.ev_k, cudaEventDisableTiming) != cudaSuccess)
+        return fail_out(cuda_fail(cudaGetLastError(), "copy-engine events"));
+    if (S.ce_bytes < sa + sb + sc) {
+        cudaDeviceSynchronize();  // the previous call may still use ce_buf
+        if (S.ce_buf) cudaFree(S.ce_buf);
+        S.ce_buf = nullptr;
+        S.ce_bytes = 0;
+        if (cudaMalloc(&S.ce_buf, sa + sb + sc) != cudaSuccess)
+            return fail_out(cuda_fail(cudaGetLastError(), "copy-engine buffer"));
+        S.ce_bytes = sa + sb + sc;
+    }
+    uint32_t *da = (uint32_t *)S.ce_buf;
+    uint32_t *db = (uint32_t *)((char *)S.ce_buf + sa);
+    uint32_t *dc = (uint32_t *)((char *)S.ce_buf + sa + sb);
+    // all three streams start after prior work on the caller's stream and
+    // after the previous call (which used the same buffers) has finished
+    if (cudaEventRecord(S.ev_start, user) != cudaSuccess ||
+        cudaStreamWaitEvent(S.s_in, S.ev_start, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(S.s_in, S.ev_done, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(S.s_cmp, S.ev_start, 0) != cudaSuccess ||
+        cudaStreamWaitEvent(S.s_out, S.ev_start, 0) != cudaSuccess)
+        return fail_out(cuda_fail(cudaGetLastError(), "copy-engine ordering"));
+    int64_t r0 = 0;
+    for (size_t i = 0; i < nch; ++i) {
+        const int64_t nr = rows[i];
+        if (cudaMemcpyAsync(da + r0 * z1, a + r0 * z1, 4ull * z1 * nr, cudaMemcpyHostToDevice,
+                            S.s_in) != cudaSuccess ||
+            cudaMemcpyAsync(db + r0 * z2, b + r0 * z2, 4ull * z2 * nr, cudaMemcpyHostToDevice,
+                            S.s_in) != cudaSuccess ||
+            cudaEventRecord(S.ce_in[i], S.s_in) != cudaSuccess ||
+            cudaStreamWaitEvent(S.s_cmp, S.ce_in[i], 0) != cudaSuccess)
+            return fail_out(cuda_fail(cudaGetLastError(), "copy-engine H2D"));
+        mc_status st = conv_dispatch(engine, da + r0 * z1, z1, z1, db + r0 * z2, z2, z2,
+                                     dc + r0 * n, n, nr, p, S.s_cmp);
+        if (st != MC_OK) return fail_out(st);
+        if (cudaEventRecord(S.ce_cmp[i], S.s_cmp) != cudaSuccess ||
+            cudaStreamWaitEvent(S.s_out, S.ce_cmp[i], 0) != cudaSuccess ||
+            cudaMemcpyAsync(c + r0 * n, dc + r0 * n, 4ull * n * nr, cudaMemcpyDeviceToHost,
+                            S.s_out) != cudaSuccess)
+            return fail_out(cuda_fail(cudaGetLastError(), "copy-engine D2H"));
+        r0 += nr;
+    }
+    if (cudaEventRecord(S.ev_k, S.s_out) != cudaSuccess ||
+        cudaStreamWaitEvent(user, S.ev_k, 0) != cudaSuccess ||
+        cudaEventRecord(S.ev_done, user) != cudaSuccess)
+        return fail_out(cuda_fail(cudaGetLastError(), "copy-engine join"));
+    *out = MC_OK;
+    return 0;
+}
+
 mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t z1,
                              const uint32_t *b, int64_t ldb, int32_t z2, uint32_t *c,
                              int64_t ldc, int64_t batch, uint32_t p, int64_t chunk_rows,
@@ -406,9 +506,9 @@ mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t
     if (lda < z1 || ldb < z2 || ldc < n) return fail(MC_EINVAL, "bad leading dimension");
     if (batch <= 0) return batch == 0 ? MC_OK : fail(MC_EINVAL, "negative batch");
     if (!a || !b || !c) return fail(MC_EINVAL, "null pointer");
+    int K = 0;
+    while ((1ll << K) < n) ++K;
     {  // validate the field / size up front (synchronous errors, nothing launched)
-        int K = 0;
-        while ((1ll << K) < n) ++K;
         const FieldTables *T;
         mc_status st = get_tables(p, K, &T);
         if (st != MC_OK) return st;
@@ -448,7 +548,12 @@ mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t
         S.in_bytes = 0;
         S.flags = nullptr;
     }
-    if (zc == 1 && c_mapped) {
+    if (zc == 3 && c_mapped && zero_copy_ok(a) && zero_copy_ok(b)) {
+        mc_status st = MC_OK;
+        if (ce_full_call(S, engine, a, lda, z1, b, ldb, z2, c, ldc, batch, p, user, &st) == 0)
+            return st;
+    }
+    if ((zc == 1 || (zc == 3 && K >= 11)) && c_mapped) {  // streamed inputs (or mode 3 n/a)
         mc_status st = MC_OK;
         if (stream_in_call(S, engine, a, lda, z1, b, ldb, z2, c, ldc, batch, p, user, &st) == 0)
             return st;

@@ -209,9 +209,10 @@ def test_host_streamed_inputs(orc, monkeypatch, engine):
     assert np.array_equal(got.numpy().view(np.uint32), want)
 
 
-@pytest.mark.parametrize("mode", ["zc", "in", "pipe"])
+@pytest.mark.parametrize("mode", ["zc", "ce", "in", "pipe"])
 def test_host_modes_forced(orc, monkeypatch, mode):
-    """Every host mode (zero copy, streamed inputs, chunked pipeline) forced
+    """Every host mode (zero copy, copy engines both ways, streamed inputs,
+    chunked pipeline) forced
     on the same batch: bit-exact products, strided rows in and out, nothing
     written past n, staging reused across calls."""
     monkeypatch.setenv("MC_HOST_MODE", mode)
@@ -236,10 +237,12 @@ def test_host_modes_forced(orc, monkeypatch, mode):
         assert (cp[:, n:] == -1).all()
 
 
-def test_host_async_calls_on_two_streams(orc):
+@pytest.mark.parametrize("mode", ["", "ce"])
+def test_host_async_calls_on_two_streams(orc, monkeypatch, mode):
     """Two asynchronous host-buffer calls on different caller streams, issued
     back to back: the second must not overwrite the first's staging."""
     from paper_1609_01010_b200 import _native
+    monkeypatch.setenv("MC_HOST_MODE", mode)
     p = P3
     B, z1, z2 = 600, 1500, 2100
     n = z1 + z2 - 1
