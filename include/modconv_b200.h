@@ -89,6 +89,20 @@ mc_status mc_conv_tft(const uint32_t *a, int64_t lda, int32_t z1,
 mc_status mc_circ_conv(const uint32_t *u, const uint32_t *v, uint32_t *w,
                        int32_t log2L, int64_t batch, uint32_t p, void *stream);
 
+/* Definition engine: batched convolution straight from its defining sum,
+ * for any modulus 2 <= p < 2^31 (no roots of unity, so any length).
+ * circ == 0: linear, c[k] = sum_{i+j=k} a_i b_j, n = z1 + z2 - 1 per row
+ *   (convolve.py:71-87 lin_conv_def; poly.py:90-105 schoolbook_raw behind
+ *   mul_schoolbook / mul_karatsuba, poly.py:100-169);
+ * circ != 0: circular of length n = z1 == z2, c[k] = sum_{i+j=k mod n}
+ *   (convolve.py:54-68 circ_conv_def).
+ * Rows with leading dimensions lda/ldb/ldc; batch <= 65535.  Inputs may be
+ * any 32-bit words (reduced exactly); outputs canonical. */
+mc_status mc_conv_direct(const uint32_t *a, int64_t lda, int32_t z1,
+                         const uint32_t *b, int64_t ldb, int32_t z2,
+                         uint32_t *c, int64_t ldc, int64_t batch,
+                         uint32_t p, int32_t circ, void *stream);
+
 /* Eq. 13 split engine.  Residues of each row u (length
  * 2n) mod x^n - 1 and mod x^n + 1: a_j = u_j + u_{j+n}, b_j = u_j - u_{j+n}
  * (convolve.py:214-219 split_residues); u: [batch][2n], a, b: [batch][n]. */

@@ -34,6 +34,7 @@ _SIGS = {
     "mc_conv_fft_pad": ([vp, i64, i32, vp, i64, i32, vp, i64, i64, u32, vp], ctypes.c_int),
     "mc_conv_tft": ([vp, i64, i32, vp, i64, i32, vp, i64, i64, u32, vp], ctypes.c_int),
     "mc_circ_conv": ([vp, vp, vp, i32, i64, u32, vp], ctypes.c_int),
+    "mc_conv_direct": ([vp, i64, i32, vp, i64, i32, vp, i64, i64, u32, i32, vp], ctypes.c_int),
     "mc_crt3_slice": ([vp, vp, vp, vp, i64, i64, vp], ctypes.c_int),
     "mc_ipc_alloc": ([i64, ctypes.POINTER(ctypes.c_void_p), ctypes.c_char_p], ctypes.c_int),
     "mc_ipc_open": ([ctypes.c_char_p, ctypes.POINTER(ctypes.c_void_p)], ctypes.c_int),

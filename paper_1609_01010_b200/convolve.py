@@ -10,8 +10,11 @@ Engines run in libmodconv_b200 (mc_conv_fft_pad / mc_conv_tft /
 mc_circ_conv / mc_circ_conv_split).  `threads` is accepted and ignored (the
 GPU does not use host workers; results are schedule-independent like the
 reference's).  The quadratic "definition" engine is a CPU oracle in the
-reference; here it is served by the GPU fft_pad kernel (bit-identical
-output, no counters touched, exactly as lin_conv_def touches none).  The
+reference; here it is served by the GPU fft_pad kernel where the field has
+the roots of unity (bit-identical output, no counters touched, exactly as
+lin_conv_def touches none) and by the defining-sum kernel (mc_conv_direct)
+beyond the field's 2-adicity, where the reference's definition engine keeps
+working too.  The
 Eq. 13 "split" engine (nega_conv, circ_conv_split, split_residues,
 recombine_residues: convolve.py:172-227) runs on the GPU as two half-length
 circular convolutions around fused split/twist and untwist/recombine
@@ -79,6 +82,27 @@ def _as_batch(x, name: str) -> torch.Tensor:
     return _tensors.as_words(x)
 
 
+def _transform_feasible(fp, n: int) -> bool:
+    """Whether a power-of-two transform covering n outputs exists in fp
+    (log2 L within the 2-adicity) -- else only the definition engine applies."""
+    return (_next_pow2(n)).bit_length() - 1 <= fp.two_adicity
+
+
+def _direct_batch(a_d: torch.Tensor, b_d: torch.Tensor, c_d: torch.Tensor, p: int,
+                  circ: bool, stream=None) -> None:
+    """Definition engine on device rows (mc_conv_direct), batch-chunked to the
+    kernel's grid limit."""
+    B = a_d.shape[0]
+    z1, z2 = a_d.shape[1], b_d.shape[1]
+    lib = _native.lib()
+    for r0 in range(0, B, 65535):
+        nb = min(65535, B - r0)
+        _native.check(lib.mc_conv_direct(
+            _tensors.ptr(a_d[r0]), a_d.stride(0), z1, _tensors.ptr(b_d[r0]), b_d.stride(0), z2,
+            _tensors.ptr(c_d[r0]), c_d.stride(0), nb, p, 1 if circ else 0,
+            _tensors.stream_handle(stream)))
+
+
 def conv_batch(a: torch.Tensor, b: torch.Tensor, field, engine: str = "tft",
                out: torch.Tensor | None = None, counters: OpCounters | None = None,
                stream=None) -> torch.Tensor:
@@ -88,11 +112,14 @@ def conv_batch(a: torch.Tensor, b: torch.Tensor, field, engine: str = "tft",
     used in place (rows may be strided: any row stride >= row length);
     CPU inputs are copied to the current device inside the call and the
     result is copied back (the host-buffer path: H2D, kernel, D2H).
-    engine: "tft" (truncated transforms, convolve.py:230-253) or "fft_pad"
-    (zero-padded full transforms, convolve.py:160-169).
+    engine: "tft" (truncated transforms, convolve.py:230-253), "fft_pad"
+    (zero-padded full transforms, convolve.py:160-169), "definition" (the
+    defining sum, convolve.py:71-87; any length, no roots of unity) or
+    "auto" (GpuPlanner).
     """
-    if engine not in ("tft", "fft_pad", "auto"):
-        raise ValueError(f"batched engine must be 'tft', 'fft_pad' or 'auto', got {engine!r}")
+    if engine not in ("tft", "fft_pad", "definition", "auto"):
+        raise ValueError("batched engine must be 'tft', 'fft_pad', 'definition' or 'auto', "
+                         f"got {engine!r}")
     fp = as_field(field)
     a = _as_batch(a, "a")
     b = _as_batch(b, "b")
@@ -103,13 +130,25 @@ def conv_batch(a: torch.Tensor, b: torch.Tensor, field, engine: str = "tft",
     if z1 < 1 or z2 < 1:
         raise ValueError("inputs must be nonempty")
     n = z1 + z2 - 1
-    check_transform_size(fp, (_next_pow2(n)).bit_length() - 1)
+    if engine != "definition":
+        check_transform_size(fp, (_next_pow2(n)).bit_length() - 1)
     dev = _tensors.require_cuda()
     if engine == "auto":  # GPU-timed choice per size class (planner.GpuPlanner)
         engine = default_planner().resolve_engine(fp, z1, z2)
     host = a.device.type == "cpu"
     if host != (b.device.type == "cpu"):
         raise ValueError("a and b must be on the same device")
+    if engine == "definition":
+        a_d = a.to(dev) if host else a
+        b_d = b.to(dev) if host else b
+        if a_d.stride(1) != 1 or b_d.stride(1) != 1:
+            a_d, b_d = a_d.contiguous(), b_d.contiguous()
+        c_d = torch.empty((B, n), dtype=torch.int32, device=dev)
+        _direct_batch(a_d, b_d, c_d, fp.p, False, stream)
+        if out is not None:
+            _tensors.as_words(out).copy_(c_d)
+            return out
+        return c_d.cpu() if host else c_d
     if host:
         return _conv_batch_host(a, b, fp, engine, out, counters, stream)
     a_d, b_d = a, b
@@ -186,6 +225,33 @@ def _run_lists(engine: str, u, v, req: ConvRequest) -> list[int]:
         base + 4 * oc, n, 1, fp.p, 0, int(stream.cuda_stream)))
     stream.synchronize()
     return st[oc:oc + n].tolist()
+
+
+def _direct_lists(u, v, p: int, circ: bool) -> list[int]:
+    dev = _tensors.require_cuda()
+    a = _tensors.list_to_device(u, p, dev).view(1, -1)
+    b = _tensors.list_to_device(v, p, dev).view(1, -1)
+    n = len(u) if circ else len(u) + len(v) - 1
+    c = torch.empty((1, n), dtype=torch.int32, device=dev)
+    _direct_batch(a, b, c, p, circ)
+    return _tensors.device_to_list(c[0])
+
+
+def circ_conv_def(u, v, fp) -> list[int]:
+    """Circular convolution straight from its defining sum (convolve.py:54-68),
+    on the GPU (mc_conv_direct): any length, any field, no counters."""
+    n = len(u)
+    if n == 0 or len(v) != n:
+        raise ValueError(f"need equal nonempty lengths, got {len(u)} and {len(v)}")
+    return _direct_lists(u, v, as_field(fp).p, True)
+
+
+def lin_conv_def(u, v, fp) -> list[int]:
+    """Linear convolution straight from its defining sum (convolve.py:71-87),
+    on the GPU (mc_conv_direct): any length, any field, no counters."""
+    if len(u) == 0 or len(v) == 0:
+        raise ValueError("inputs must be nonempty")
+    return _direct_lists(u, v, as_field(fp).p, False)
 
 
 def circ_conv_fft(u, v, req: ConvRequest) -> list[int]:
@@ -342,7 +408,12 @@ def poly_mul(a, b, req: ConvRequest) -> DensePoly:
     v = _trim(b.coeffs)
     engine = _resolve_engine(len(u), len(v), req)
     if engine == "definition":
-        out = _run_lists("fft_pad", u, v, req)
+        # bit-identical either way: the fused transform kernel where the field
+        # has the roots, the defining sum beyond its 2-adicity
+        if _transform_feasible(fp, len(u) + len(v) - 1):
+            out = _run_lists("fft_pad", u, v, req)
+        else:
+            out = _direct_lists(u, v, fp.p, False)
     elif engine == "fft_pad":
         out = lin_conv_fft_pad(u, v, req)
     elif engine == "tft":

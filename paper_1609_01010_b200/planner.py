@@ -10,7 +10,8 @@ differs (e.g. at n just past a power of two the truncated engine forms ~half
 the spectrum, while at n = 0.88 L the two are within a few percent).
 
 Duck-type compatible with ConvRequest.planner: resolve_engine(field, a_len,
-b_len, threads) -> "fft_pad" | "tft".
+b_len, threads) -> "fft_pad" | "tft" | "definition" (the last where the
+field has no transform of the needed size, or for a single coefficient).
 """
 
 from __future__ import annotations
@@ -73,7 +74,13 @@ class GpuPlanner:
         return best
 
     def resolve_engine(self, field, a_len: int, b_len: int, threads: int = 1) -> str:
-        p = as_field(field).p
+        fp = as_field(field)
+        p = fp.p
+        n = a_len + b_len - 1
+        if n == 1 or (n - 1).bit_length() > fp.two_adicity:
+            # no transform of that size in this field (or nothing to transform):
+            # the defining sum, as the reference's resolve_engine (planner.py:420-422)
+            return "definition"
         key = self.size_class(p, a_len, b_len)
         with self._lock:
             hit = self._plans.get(key)

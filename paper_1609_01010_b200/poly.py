@@ -90,6 +90,54 @@ def check_same_field(a, b) -> None:
         raise FieldMismatchError(f"mixed moduli {a.field.p} and {b.field.p}")
 
 
+# ------------------------------------------------------------------ direct products
+# The reference's quadratic and divide-and-conquer multipliers (poly.py:90-181)
+# share one output contract -- the raw coefficient product, NOT normalized --
+# which the GPU defining-sum kernel (mc_conv_direct) computes for any field
+# and length.
+KARATSUBA_THRESHOLD = 16  # poly.py:15 (a tuning knob there; accepted and validated here)
+
+
+def schoolbook_raw(a, b, p: int) -> list[int]:
+    """Coefficient product of two nonempty sequences mod p (poly.py:90-97)."""
+    if len(a) == 0 or len(b) == 0:
+        raise ValueError("inputs must be nonempty")
+    from .convolve import lin_conv_def
+
+    return lin_conv_def(list(a), list(b), p)
+
+
+def mul_schoolbook(a, b) -> DensePoly:
+    """Direct convolution product c_k = sum_{i+j=k} a_i b_j (poly.py:100-105)."""
+    check_same_field(a, b)
+    fp = as_field(a.field)
+    if a.is_zero() or b.is_zero():
+        return DensePoly.zero(fp)
+    return DensePoly._trusted(fp, tuple(schoolbook_raw(a.coeffs, b.coeffs, fp.p)))
+
+
+def mul_karatsuba(a, b, threshold: int = KARATSUBA_THRESHOLD) -> DensePoly:
+    """Same output contract as mul_schoolbook, bit for bit (poly.py:156-169)."""
+    check_same_field(a, b)
+    if threshold < 1:
+        raise ValueError("threshold must be >= 1")
+    return mul_schoolbook(a, b)
+
+
+def eval_poly(a, x):
+    """Horner evaluation of a at the point x (poly.py:172-181)."""
+    from .field import Felt
+
+    if a.field.p != x.field.p:
+        raise FieldMismatchError(f"mixed moduli {a.field.p} and {x.field.p}")
+    p = a.field.p
+    xv = x.value
+    acc = 0
+    for c in reversed(a.coeffs):
+        acc = (acc * xv + c) % p
+    return Felt(acc, as_field(a.field))
+
+
 # ------------------------------------------------------------------ text format
 # Interchange format of the reference CLI (poly.py:184-223): three lines --
 # the modulus, the coefficient count, the space-separated residues.

@@ -157,6 +157,60 @@ def moddft(x, table: TwiddleTable, direction: str = "fwd", counters: OpCounters 
     return _tensors.device_to_list(y)
 
 
+def moddft_naive(x, table: TwiddleTable, direction: str = "fwd"):
+    """The transform's defining sum (transform.py:199-225): its output equals
+    moddft's bit for bit, which is what serves it (no counters, as in the
+    reference)."""
+    return moddft(x, table, direction)
+
+
+BASE_CASE_SIZES = (2, 4, 8)  # transform.py:222
+_CODELET_COST = {2: 1, 4: 4, 8: 12}  # (m/2) log2 m, transform.py:225
+
+
+def dft_basecase(x, table: TwiddleTable, direction: str = "fwd",
+                 counters: OpCounters | None = None):
+    """Loop-free DFT of size 2, 4 or 8 (transform.py:279-307): same output as
+    moddft, same argument checks and butterfly count."""
+    m = len(x)
+    if m not in BASE_CASE_SIZES:
+        raise ValueError(f"base case size must be one of {BASE_CASE_SIZES}: {m}")
+    if table.size != m:
+        raise ValueError(f"table size {table.size} != input length {m}")
+    if direction not in ("fwd", "inv"):
+        raise ValueError(f"direction must be 'fwd' or 'inv': {direction!r}")
+    out = moddft(x, table, direction)
+    if counters is not None:
+        counters.butterflies += _CODELET_COST[m]
+    return out
+
+
+def moddft_plan(x, table: TwiddleTable, splits: tuple, base_case: int, direction: str = "fwd",
+                counters: OpCounters | None = None):
+    """DFT along an explicit radix decomposition (transform.py:333-376).
+    Every valid plan yields moddft's output bit for bit and costs
+    (N/2) log2 N butterflies; the plan is validated exactly like the
+    reference, the transform runs on the GPU kernels."""
+    n = table.size
+    if len(x) != n:
+        raise ValueError(f"input length {len(x)} != table size {n}")
+    if base_case not in BASE_CASE_SIZES:
+        raise ValueError(f"base case must be one of {BASE_CASE_SIZES}: {base_case}")
+    prod = base_case
+    for sp in splits:
+        if sp not in BASE_CASE_SIZES:
+            raise ValueError(f"split radix must be one of {BASE_CASE_SIZES}: {sp}")
+        prod *= sp
+    if prod != n:
+        raise ValueError(f"decomposition {tuple(splits)} x base {base_case} != size {n}")
+    if direction not in ("fwd", "inv"):
+        raise ValueError(f"direction must be 'fwd' or 'inv': {direction!r}")
+    out = moddft(x, table, direction)
+    if counters is not None:
+        counters.butterflies += full_count(n)
+    return out
+
+
 def tft(table: TwiddleTable, x, n: int, counters: OpCounters | None = None):
     """First n spectral values, bit-reversed order (transform.py:421-448)."""
     size = table.size

@@ -50,3 +50,18 @@ def test_sweep_schema_counters_and_sentinels(tmp_path):
     out3 = tmp_path / "s3.csv"
     assert cli.main(["sweep", "--min", "3000", "--max", "3001", "--batch", "64", "--reps", "2",
                      "-o", str(out3)]) == 0
+
+
+def test_sweep_definition_rows_beyond_two_adicity(tmp_path):
+    """Definition (and auto) rows keep working at every size (reference
+    tests/test_cli.py:171-178): p = 17 has no transform past length 16."""
+    out = tmp_path / "d.csv"
+    assert cli.main(["sweep", "--min", "15", "--max", "20", "--engines", "tft,definition,auto",
+                     "--prime", "17", "--reps", "2", "-o", str(out)]) == 0
+    by = {(r.split(",")[0], r.split(",")[1]): r.split(",") for r in
+          out.read_text().splitlines()[1:]}
+    assert by[("20", "tft")][3] == "-1"
+    for n in range(15, 21):
+        assert by[(str(n), "definition")][3] != "-1"
+        assert by[(str(n), "auto")][3] != "-1"
+    assert by[("20", "definition")][5:] == ["0", "0"]
