@@ -65,3 +65,27 @@ def test_sweep_definition_rows_beyond_two_adicity(tmp_path):
         assert by[(str(n), "definition")][3] != "-1"
         assert by[(str(n), "auto")][3] != "-1"
     assert by[("20", "definition")][5:] == ["0", "0"]
+
+
+def test_plan_and_mul_auto_store(tmp_path):
+    """`plan` writes a modconv-plan v1 store (dft/tft planned, itft mirrored);
+    `mul --engine auto --store` reuses and extends it (cli.py:95-171)."""
+    store = tmp_path / "plans.txt"
+    assert cli.main(["plan", "--store", str(store), "--max-l", "64"]) == 0
+    st = mc.store_load(str(store))
+    assert len(st) == 3 * 6
+    kinds = sorted({e.key.kind for e in st})
+    assert kinds == ["dft", "itft", "tft"]
+    assert cli.main(["plan", "--store", str(store), "--max-l", "48"]) == cli.EXIT_USAGE
+    assert cli.main(["plan", "--store", str(store), "--max-l", "64", "--prime", "17"]) == \
+        cli.EXIT_UNSUPPORTED
+    a = tmp_path / "a.txt"
+    a.write_text("998244353\n5\n1 2 3 4 5\n")
+    out = tmp_path / "c.txt"
+    assert cli.main(["mul", str(a), str(a), "--store", str(store), "-o", str(out)]) == 0
+    assert mc.poly_from_text(out.read_text()).coeffs == (1, 4, 10, 20, 35, 44, 46, 40, 25)
+    assert len(mc.store_load(str(store))) >= len(st)
+    bad = tmp_path / "bad.txt"
+    bad.write_text("not a store\n")
+    assert cli.main(["mul", str(a), str(a), "--store", str(bad), "-o", str(out)]) == \
+        cli.EXIT_FILE_FORMAT
