@@ -275,3 +275,38 @@ def test_list_api_poly_mul(golden_small):
                         mc.ConvRequest(fp, engine=c["engine"], counters=cnt))
         assert list(r.coeffs) == c["out"]
         assert [cnt.butterflies, cnt.pointwise_muls] == c["counters"]
+
+
+def test_concurrent_host_threads(orc):
+    """Engines are reentrant (reference SPEC: pure, per-call counters): eight
+    host threads multiplying at once on one device, list and tensor APIs,
+    three fields (tables built concurrently), results bit-exact."""
+    import threading
+
+    results, errors = {}, []
+
+    def work(k):
+        try:
+            p = (P1, P2, P3)[k % 3]
+            fp = mc.FourierPrime.from_modulus(p)
+            a = orc.gen_u32(80 + k, 0, 0, 6, 700 + 37 * k, p)
+            b = orc.gen_u32(80 + k, 1, 0, 6, 500 + 11 * k, p)
+            want = orc.conv_batch(a, b, p, 1)[0]
+            got = mc.conv_batch(torch.from_numpy(a.view(np.int32)).cuda(),
+                                torch.from_numpy(b.view(np.int32)).cuda(), p, engine="tft")
+            torch.cuda.synchronize()
+            cnt = mc.OpCounters()
+            r = mc.poly_mul(mc.DensePoly(fp, tuple(a[0].tolist())), mc.DensePoly(fp, tuple(b[0].tolist())),
+                            mc.ConvRequest(fp, engine="fft_pad", counters=cnt))
+            results[k] = (np.array_equal(got.cpu().numpy().view(np.uint32), want),
+                          list(r.coeffs) == want[0][:len(r.coeffs)].tolist())
+        except Exception as exc:  # noqa: BLE001
+            errors.append(repr(exc))
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(8)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    assert all(all(v) for v in results.values()) and len(results) == 8
