@@ -135,6 +135,11 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
         return MC_OK;
     }
     if (K <= kSmallMaxK) {
+        if (z1 > z2) {  // the kernel folds L^-1 into operand a: make it the shorter one
+            std::swap(a, b);
+            std::swap(lda, ldb);
+            std::swap(z1, z2);
+        }
         ConvSmallParams P = make_params(T, a, lda, z1, b, ldb, z2, c, ldc, n, batch);
         P.reduce = reduce ? 1 : 0;
         P.red_wp = (u32)((1ull << 32) / p);

@@ -112,11 +112,20 @@ struct Tw {
 // zeros are real zeros in the registers, so the result is exact).  No
 // runtime branch splits the unrolled butterflies, so ptxas can interleave
 // the independent chains.
-template <int K, int NT, int ZS, int AR = 0>
+// SCALE: the operand is multiplied by L^-1 * 2^32 on its ZS possibly non-zero
+// slots first (the product is linear in each operand), so the pointwise
+// step is a bare Montgomery product.  The kernel always scales operand a,
+// which the host makes the shorter one: at most 8 slots per thread against
+// the >= 9 active slots of the pointwise step.
+template <int K, int NT, int ZS, int AR = 0, bool SCALE = false>
 __device__ __forceinline__ void fwd_top_zs(u32 (&v)[16], int t, const ConvSmallParams &P,
                                            const Tw &W) {
     constexpr int G = 1 << (K - 4);
     const u32 p = P.p;
+    if constexpr (SCALE) {
+#pragma unroll
+        for (int s = 0; s < ZS; ++s) v[s] = mul_t<AR>(v[s], P.linv_mont, p);
+    }
 #pragma unroll
     for (int lv = 3; lv >= 0; --lv) {
         const int H = 1 << lv;
@@ -151,30 +160,36 @@ __device__ __forceinline__ void fwd_top_zs(u32 (&v)[16], int t, const ConvSmallP
 #define MC_ZS_STEP 4
 #endif
 
-template <int K, int NT, int AR = 0>
+template <int K, int NT, int AR = 0, bool SCALE = false>
 __device__ __forceinline__ void fwd_top(u32 (&v)[16], int z, int t, const ConvSmallParams &P,
                                         const Tw &W) {
     constexpr int G = 1 << (K - 4);
     const int zs = (z + G - 1) / G;  // uniform across the launch
 #if MC_ZS_STEP == 2
-    if (zs <= 2) fwd_top_zs<K, NT, 2, AR>(v, t, P, W);
-    else if (zs <= 4) fwd_top_zs<K, NT, 4, AR>(v, t, P, W);
-    else if (zs <= 6) fwd_top_zs<K, NT, 6, AR>(v, t, P, W);
-    else if (zs <= 8) fwd_top_zs<K, NT, 8, AR>(v, t, P, W);
-    else if (zs <= 10) fwd_top_zs<K, NT, 10, AR>(v, t, P, W);
-    else if (zs <= 12) fwd_top_zs<K, NT, 12, AR>(v, t, P, W);
-    else if (zs <= 14) fwd_top_zs<K, NT, 14, AR>(v, t, P, W);
-    else fwd_top_zs<K, NT, 16, AR>(v, t, P, W);
+    if (zs <= 2) fwd_top_zs<K, NT, 2, AR, SCALE>(v, t, P, W);
+    else if (zs <= 4) fwd_top_zs<K, NT, 4, AR, SCALE>(v, t, P, W);
+    else if (zs <= 6) fwd_top_zs<K, NT, 6, AR, SCALE>(v, t, P, W);
+    else if (zs <= 8) fwd_top_zs<K, NT, 8, AR, SCALE>(v, t, P, W);
+    else if (zs <= 10) fwd_top_zs<K, NT, 10, AR, SCALE>(v, t, P, W);
+    else if (zs <= 12) fwd_top_zs<K, NT, 12, AR, SCALE>(v, t, P, W);
+    else if (zs <= 14) fwd_top_zs<K, NT, 14, AR, SCALE>(v, t, P, W);
+    else fwd_top_zs<K, NT, 16, AR, SCALE>(v, t, P, W);
 #elif MC_ZS_STEP == 4
-    if (zs <= 4) fwd_top_zs<K, NT, 4, AR>(v, t, P, W);
-    else if (zs <= 8) fwd_top_zs<K, NT, 8, AR>(v, t, P, W);
-    else if (zs <= 12) fwd_top_zs<K, NT, 12, AR>(v, t, P, W);
-    else fwd_top_zs<K, NT, 16, AR>(v, t, P, W);
+    if (zs <= 4) fwd_top_zs<K, NT, 4, AR, SCALE>(v, t, P, W);
+    else if (zs <= 8) fwd_top_zs<K, NT, 8, AR, SCALE>(v, t, P, W);
+    else if (zs <= 12) fwd_top_zs<K, NT, 12, AR, SCALE>(v, t, P, W);
+    else fwd_top_zs<K, NT, 16, AR, SCALE>(v, t, P, W);
 #else
-    if (zs <= 8) fwd_top_zs<K, NT, 8, AR>(v, t, P, W);
-    else fwd_top_zs<K, NT, 16, AR>(v, t, P, W);
+    if (zs <= 8) fwd_top_zs<K, NT, 8, AR, SCALE>(v, t, P, W);
+    else fwd_top_zs<K, NT, 16, AR, SCALE>(v, t, P, W);
 #endif
 }
+
+// L^-1 folded into operand a at the top pass (fwd_top_zs SCALE) instead of
+// the pointwise step; MC_PRESCALE=0 restores the pointwise scaling (A/B).
+#ifndef MC_PRESCALE
+#define MC_PRESCALE 1
+#endif
 
 // ---------------------------------------------------------------- lower passes
 template <int K, int LO, int HI, int SB, int AR = 0>
@@ -579,12 +594,12 @@ conv_small_kernel(const ConvSmallParams P) {
         if ((FL & FL_REDUCE) && P.reduce) {  // three-primes inputs: any 32-bit word -> residue
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
-                va[s] = mul_t<AR>(va[s], 1u, P.red_wp, P.p);
+                if (!MC_PRESCALE) va[s] = mul_t<AR>(va[s], 1u, P.red_wp, P.p);  // else: scaling reduces
                 vb[s] = mul_t<AR>(vb[s], 1u, P.red_wp, P.p);
             }
         }
 
-        fwd_top<K, NT, AR>(va, P.z1, t, P, W);
+        fwd_top<K, NT, AR, MC_PRESCALE != 0>(va, P.z1, t, P, W);
         fwd_top<K, NT, AR>(vb, P.z2, t, P, W);
         // the previous product's bulk store has read its staging before the
         // first exchange (after the barrier inside the chain) reuses bufA
@@ -600,7 +615,9 @@ conv_small_kernel(const ConvSmallParams P) {
                 if ((slot_pos<SB>(t, 0) >> (K - 4)) < NT) {
 #pragma unroll
                     for (int s = 0; s < 16; ++s)
-                        va[s] = mul_inv_t<AR>(mont_mul(va[s], vb[s], P.p, P.pinv), P.linv_mont, P.p);
+                        va[s] = MC_PRESCALE ? mont_mul(va[s], vb[s], P.p, P.pinv)
+                                            : mul_inv_t<AR>(mont_mul(va[s], vb[s], P.p, P.pinv),
+                                                            P.linv_mont, P.p);
                 } else {
 #pragma unroll
                     for (int s = 0; s < 16; ++s) va[s] = 0u;  // inactive tail: u_j = 0
@@ -610,7 +627,9 @@ conv_small_kernel(const ConvSmallParams P) {
                 for (int s = 0; s < 16; ++s) {
                     const int x = slot_pos<SB>(t, s);
                     if (NT >= 16 || (x >> (K - 4)) < NT)
-                        va[s] = mul_inv_t<AR>(mont_mul(va[s], vb[s], P.p, P.pinv), P.linv_mont, P.p);
+                        va[s] = MC_PRESCALE ? mont_mul(va[s], vb[s], P.p, P.pinv)
+                                            : mul_inv_t<AR>(mont_mul(va[s], vb[s], P.p, P.pinv),
+                                                            P.linv_mont, P.p);
                     else
                         va[s] = 0u;  // time values of the inactive tail: u_j = 0
                 }
