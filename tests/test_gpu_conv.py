@@ -92,6 +92,28 @@ def test_power_of_two_boundaries(orc, L, p):
                 assert np.array_equal(_conv(a, b, p, eng), want), (p, n, z1, eng)
 
 
+@pytest.mark.parametrize("K", list(range(4, 14)))
+@pytest.mark.parametrize("p", [P1, P3])
+def test_fused_and_latency_paths_every_size(orc, K, p):
+    """The fused kernel at every size with batches of 1, 40 and 300 (one CTA
+    per product, a partial wave, more products than resident CTAs on the
+    smaller sizes) -- same rows, bit-exact vs the oracle, at n = L and n just
+    past L/2 (truncated transform), all-(p-1) rows."""
+    L = 1 << K
+    for n in (L, L // 2 + 1):
+        z1 = (n + 1) // 3 + 1
+        z2 = n + 1 - z1
+        a = orc.gen_u32(14, 0, K * 10 + (n == L), 300, z1, p)
+        b = orc.gen_u32(14, 1, K * 10 + (n == L), 300, z2, p)
+        a[0, :] = p - 1
+        b[0, :] = p - 1
+        want, _, _ = orc.conv_batch(a, b, p, 1, threads=8)
+        for eng in ("fft_pad", "tft"):
+            for B in (1, 40, 300):
+                got = _conv(a[:B], b[:B], p, eng)
+                assert np.array_equal(got, want[:B]), (K, n, eng, B)
+
+
 def test_cfg1_single_product(golden_configs):
     for cfg in golden_configs["configs"]:
         if cfg["cfg"] != 1:
