@@ -433,12 +433,13 @@ def run_mine(args, cfg):
         alg_bytes = 4 * (z1 + z2 + n) * B
         bytes_note = "compulsory 4*(z1+z2+n) per product (fused single pass)"
     kern_ms = statistics.mean(times)  # one launch of the fused kernel per step (cfg 1-3)
-    traffic = None
-    try:  # DRAM bytes per launch from the committed ncu capture of this workload
+    traffic, ncu_pipes = None, None
+    try:  # DRAM bytes and pipe utilisation per launch from the committed ncu capture
         with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
             tr = json.load(f).get(cfg["name"])
         if tr:
             traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+            ncu_pipes = tr.get("ncu_pipes")
     except Exception:
         traffic = None
     achieved = alg_bytes / (kern_ms / 1e3) / 1e9
@@ -468,7 +469,8 @@ def run_mine(args, cfg):
                      "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
                      "alg_bytes_per_step": alg_bytes, "bytes_model": bytes_note,
                      "kernel_ms": kern_ms},
-        "int_pipe": _int_roofline(bf, pw, value / ws, peaks, lazy_share(cfg)),
+        "int_pipe": dict(_int_roofline(bf, pw, value / ws, peaks, lazy_share(cfg)),
+                         **({"ncu": ncu_pipes} if ncu_pipes else {})),
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clk,
