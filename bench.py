@@ -405,15 +405,17 @@ def run_mine(args, cfg):
         mc.mul_three_primes_tensor(a_h, b_h, out=c).cpu()
         torch.cuda.synchronize()
         barrier()
-        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        s0.record(stream)
-        for _ in range(args.steps):
+        ev3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
+        for i in range(args.steps):
             flush.zero_()
+            ev3[i][0].record(stream)
             cc = mc.mul_three_primes_tensor(a_h, b_h, out=c)
             c_h.copy_(cc, non_blocking=True)
-        s1.record(stream)
+            ev3[i][1].record(stream)
         barrier()
-        e2e = {"value": args.steps / (s0.elapsed_time(s1) / 1e3), "unit": "products/s",
+        t3 = sum(s.elapsed_time(e) for s, e in ev3)
+        e2e = {"value": args.steps / (t3 / 1e3), "unit": "products/s",
                "h2d_bytes_per_step": 4 * (z1 + z2), "d2h_bytes_per_step": 12 * n}
 
     if rank != 0:

@@ -28,7 +28,9 @@ MODULUS = PRIMES[0] * PRIMES[1] * PRIMES[2]
 def _dev_words(x, device) -> torch.Tensor:
     if isinstance(x, torch.Tensor):
         t = _tensors.as_words(x.reshape(-1))
-        return t.to(device).contiguous()
+        # page-locked host rows: a stream-ordered copy, so the host goes on to
+        # enqueue the transforms while the copy engine runs
+        return t.to(device, non_blocking=t.device.type == "cpu" and t.is_pinned()).contiguous()
     vals = [int(v) for v in x]
     if any(v < 0 or v >= (1 << 32) for v in vals):
         raise ValueError("three-primes inputs must be integers in [0, 2^32)")
