@@ -295,7 +295,7 @@ struct RowsParams {
     const uint2 *tf;  // tf[h + j] = w_{2h}^j (Shoup pairs)
     const uint2 *ti;  // ti[h + j] = w_{2h}^-j
     // itft: the partial path of the van der Hoeven recursion, top-down
-    int nc;
+    int nc, nbig;  // chain nodes; the first nbig have h > 32 (CTA-wide), the rest run on one warp
     int c_off[kChainMax], c_h[kChainMax], c_n[kChainMax];
     Shoup c_mm[kChainMax], c_ih[kChainMax];  // m mod p, h^-1 mod p of each node
 };
@@ -312,6 +312,37 @@ struct PadRow {
         return s[y + (y >> 4)];
     }
 };
+
+// NB inverse DIT stages (h = S .. S 2^(NB-1)) in registers on each of the
+// `full` aligned S 2^NB-chunks at the start of the row: item k = (chunk,
+// offset o < S) holds the 2^NB elements chunk*S 2^NB + o + q S.
+template <int NB>
+__device__ __forceinline__ void dit_reg_pass(const PadRow &s, const uint2 *ti, int S, int lgS,
+                                             int full, int tid, int nth, u32 p) {
+    constexpr int E = 1 << NB;
+    for (int k = tid; k < (full << lgS); k += nth) {
+        const int o = k & (S - 1);
+        const PadRow base{s.s, ((k >> lgS) << (lgS + NB)) + o};
+        u32 v[E];
+#pragma unroll
+        for (int q = 0; q < E; ++q) v[q] = base[q * S];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) {
+            const int hh = S << b;
+#pragma unroll
+            for (int q = 0; q < E; ++q) {
+                if (q & (1 << b)) continue;
+                const int j = (q & ((1 << b) - 1)) * S + o;
+                const u32 t = mul_tw(v[q + (1 << b)], __ldg(ti + hh + j), p);
+                const u32 a = v[q];
+                v[q] = add_mod(a, t, p);
+                v[q + (1 << b)] = sub_mod(a, t, p);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < E; ++q) base[q * S] = v[q];
+    }
+}
 
 // MODE 0: tft (transform.py:379-418, levels top-down, pruned by z and n);
 // MODE 1: itft (transform.py:451-489): the complete sub-blocks of the
@@ -332,14 +363,14 @@ __global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
         __syncthreads();
         if (MODE == 0) {
             for (int h = L >> 1; h >= 1; h >>= 1) {
-                const int m = 2 * h;
+                const int m = 2 * h, lgh = __ffs(h) - 1;
                 const int nblk = (n + m - 1) / m;
                 const int zz = P.z < m ? P.z : m;
                 const int per = nblk * h;
                 for (int k = tid; k < per; k += NTH) {
                     const int j = k & (h - 1);
                     if (j >= zz) continue;
-                    const int lo = (k / h) * m + j, hi = lo + h;
+                    const int lo = ((k >> lgh) << (lgh + 1)) + j, hi = lo + h;
                     const bool b_zero = j + h >= zz;
                     if (lo - j + h < n) {  // hi output needed
                         const uint2 w = __ldg(P.tf + h + j);
@@ -358,46 +389,31 @@ __global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
             }
         } else {
             // 1. complete blocks: inverse DIT, stage h over the aligned 2h-chunks
-            // below n.  Four stages at a time (h = S .. 8S, S = 16^q) run in
-            // registers on the aligned 16S-chunks below n (16 elements at
-            // stride S per thread); the tail [16S * floor(n / 16S), n) runs
-            // those stages one at a time.  Leftover top stages (K mod 4) and
-            // all stages with no complete 16S-chunk run one at a time.
-            int h = 1;
-            for (int S = 1; 16 * S <= L; S *= 16) {
-                const int CH = 16 * S, full = n / CH;
-                if (full == 0) break;
-                const int lgS = __ffs(S) - 1;
-                for (int k = tid; k < full * S; k += NTH) {
-                    const PadRow base{s.s, (k >> lgS) * CH + (k & (S - 1))};
-                    const int o = k & (S - 1);
-                    u32 v[16];
-#pragma unroll
-                    for (int q = 0; q < 16; ++q) v[q] = base[q * S];
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) {
-                        const int hh = S << b;
-#pragma unroll
-                        for (int q = 0; q < 16; ++q) {
-                            if (q & (1 << b)) continue;
-                            const int j = (q & ((1 << b) - 1)) * S + o;
-                            const u32 t = mul_tw(v[q + (1 << b)], __ldg(P.ti + hh + j), p);
-                            const u32 a = v[q];
-                            v[q] = add_mod(a, t, p);
-                            v[q + (1 << b)] = sub_mod(a, t, p);
-                        }
-                    }
-#pragma unroll
-                    for (int q = 0; q < 16; ++q) base[q * S] = v[q];
+            // below n.  NB <= 4 stages at a time (h = S .. S 2^(NB-1)) run in
+            // registers on the aligned S 2^NB-chunks below n (2^NB elements at
+            // stride S per thread), NB the most stages that still have a
+            // complete chunk; the tail [chunks, n) runs those stages one at a
+            // time.  When no chunk of two stages' size fits, no stage is left.
+            for (int h = 1; h < L;) {
+                const int lgS = __ffs(h) - 1;
+                int nb = min(4, P.K - lgS);
+                while (nb > 0 && (n >> (lgS + nb)) == 0) --nb;
+                if (nb == 0) break;
+                const int full = n >> (lgS + nb);
+                switch (nb) {
+                    case 4: dit_reg_pass<4>(s, P.ti, h, lgS, full, tid, NTH, p); break;
+                    case 3: dit_reg_pass<3>(s, P.ti, h, lgS, full, tid, NTH, p); break;
+                    case 2: dit_reg_pass<2>(s, P.ti, h, lgS, full, tid, NTH, p); break;
+                    default: dit_reg_pass<1>(s, P.ti, h, lgS, full, tid, NTH, p); break;
                 }
                 // tail stages (disjoint from the chunks above)
-                for (int b = 0; b < 4; ++b) {
-                    const int hh = S << b;
-                    const int k0 = full * CH / 2, per = (n / (2 * hh)) * hh;
+                for (int b = 0; b < nb; ++b) {
+                    const int hh = h << b, lgh = lgS + b;
+                    const int k0 = (full << (lgS + nb)) >> 1, per = (n >> (lgh + 1)) << lgh;
                     if (per > k0) {
                         for (int k = k0 + tid; k < per; k += NTH) {
                             const int j = k & (hh - 1);
-                            const int lo = (k / hh) * 2 * hh + j, hi = lo + hh;
+                            const int lo = ((k >> lgh) << (lgh + 1)) + j, hi = lo + hh;
                             const u32 t = mul_tw(s[hi], __ldg(P.ti + hh + j), p);
                             const u32 a = s[lo];
                             s[lo] = add_mod(a, t, p);
@@ -407,44 +423,33 @@ __global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
                     }
                 }
                 __syncthreads();
-                h = 16 * S;
+                h <<= nb;
             }
-            for (; h < L; h <<= 1) {
-                const int per = (n / (2 * h)) * h;
-                if (per == 0) break;
-                for (int k = tid; k < per; k += NTH) {
-                    const int j = k & (h - 1);
-                    const int lo = (k / h) * 2 * h + j, hi = lo + h;
-                    const u32 t = mul_tw(s[hi], __ldg(P.ti + h + j), p);
-                    const u32 a = s[lo];
-                    s[lo] = add_mod(a, t, p);
-                    s[hi] = sub_mod(a, t, p);
-                }
-                __syncthreads();
-            }
-            // 2. down the partial path: cross butterflies (n > h) or pre-adds
-            for (int c = 0; c < P.nc; ++c) {
+            // 2./3. the partial path: down (cross butterflies where n > h, else
+            // pre-adds), then up (DIT butterflies / combines).  Nodes with
+            // h > 32 run on the whole CTA, one barrier each; the small nodes at
+            // the bottom of the path (a region of <= 64 elements) run on warp 0
+            // between two warp barriers, down and back up without a CTA barrier.
+            auto node_down = [&](int c, int first, int step) {
                 const int off = P.c_off[c], h = P.c_h[c], nn = P.c_n[c];
                 const PadRow row{s.s, off};
                 if (nn > h) {
                     const Shoup mm = P.c_mm[c], ih = P.c_ih[c];
-                    for (int i = nn - h + tid; i < h; i += NTH) {
+                    for (int i = nn - h + first; i < h; i += step) {
                         const u32 a = row[i], b = row[i + h];
                         const u32 d = sub_mod(mul_shoup(a, ih, p), add_mod(b, b, p), p);
                         row[i + h] = mul_tw(d, __ldg(P.tf + h + i), p);
                         row[i] = sub_mod(add_mod(a, a, p), mul_shoup(b, mm, p), p);
                     }
                 } else {
-                    for (int i = nn + tid; i < h; i += NTH) row[i] = add_mod(row[i], row[i + h], p);
+                    for (int i = nn + first; i < h; i += step) row[i] = add_mod(row[i], row[i + h], p);
                 }
-                __syncthreads();
-            }
-            // 3. up the partial path: DIT butterflies (n > h) or combines
-            for (int c = P.nc - 1; c >= 0; --c) {
+            };
+            auto node_up = [&](int c, int first, int step) {
                 const int off = P.c_off[c], h = P.c_h[c], nn = P.c_n[c];
                 const PadRow row{s.s, off};
                 if (nn > h) {
-                    for (int i = tid; i < nn - h; i += NTH) {
+                    for (int i = first; i < nn - h; i += step) {
                         const u32 t = mul_tw(row[i + h], __ldg(P.ti + h + i), p);
                         const u32 a = row[i];
                         row[i] = add_mod(a, t, p);
@@ -452,11 +457,31 @@ __global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
                     }
                 } else {
                     const Shoup mm = P.c_mm[c];
-                    for (int i = tid; i < nn; i += NTH) {
+                    for (int i = first; i < nn; i += step) {
                         const u32 a = row[i];
                         row[i] = sub_mod(add_mod(a, a, p), mul_shoup(row[i + h], mm, p), p);
                     }
                 }
+            };
+            for (int c = 0; c < P.nbig; ++c) {
+                node_down(c, tid, NTH);
+                __syncthreads();
+            }
+            if (P.nbig < P.nc) {
+                if (tid < 32) {
+                    for (int c = P.nbig; c < P.nc; ++c) {
+                        node_down(c, tid, 32);
+                        __syncwarp();
+                    }
+                    for (int c = P.nc - 1; c >= P.nbig; --c) {
+                        node_up(c, tid, 32);
+                        __syncwarp();
+                    }
+                }
+                __syncthreads();
+            }
+            for (int c = P.nbig - 1; c >= 0; --c) {
+                node_up(c, tid, NTH);
                 __syncthreads();
             }
         }
@@ -501,6 +526,7 @@ static mc_status rows_launch(int mode, const u32 *x, long long ldx, int z, u32 *
             }
             m = h;
         }
+        while (R.nbig < R.nc && R.c_h[R.nbig] > 32) ++R.nbig;
     }
     const int L = 1 << K;
     const int threads = std::max(32, std::min(512, L / 16));
