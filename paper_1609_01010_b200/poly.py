@@ -3,8 +3,9 @@
 Mirrors the reference's DensePoly (/root/reference/pkg/src/modconv/poly.py:
 26-82), the input/output type of poly_mul: an immutable (field, coeffs) pair
 with every coefficient a canonical residue, trailing zeros allowed and
-stripped by normalize().  The classical O(n^2) multipliers of the reference
-are test oracles and live under oracle/, not here.
+stripped by normalize().  The reference's classical multipliers
+(mul_schoolbook / mul_karatsuba, poly.py:90-169) run on the GPU's
+defining-sum kernel (mc_conv_direct); eval_poly is host-side Horner.
 """
 
 from __future__ import annotations
