@@ -102,6 +102,33 @@ def _int_roofline(bf: int, pw: int, products_per_s_per_gpu: float, peaks: dict,
     return out
 
 
+def _bind_local_cpus(dev_index: int):
+    """Pin this rank to the CPU cores local to its GPU (NVML affinity), so the
+    page-locked buffers of the e2e leg are allocated on the GPU's NUMA node
+    and zero-copy / copy-engine traffic does not cross the socket
+    interconnect.  Returns the previous affinity (restored for the CPU
+    baseline), or None when NVML or the mapping is unavailable."""
+    try:
+        import pynvml
+        import torch
+
+        prop = torch.cuda.get_device_properties(dev_index)
+        pynvml.nvmlInit()
+        bus = f"{prop.pci_domain_id:08x}:{prop.pci_bus_id:02x}:{prop.pci_device_id:02x}.0"
+        h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        ncpu = os.cpu_count() or 1
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (ncpu + 63) // 64)
+        cpus = {64 * w + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        old = set(os.sched_getaffinity(0))
+        cpus &= old
+        if cpus and cpus != old:
+            os.sched_setaffinity(0, cpus)
+            return old
+    except Exception:
+        pass
+    return None
+
+
 def _coll_device(dev):
     """Device for collective tensors: the GPU under NCCL, the host under gloo."""
     import torch.distributed as dist
@@ -266,6 +293,7 @@ def run_mine(args, cfg):
             dist.init_process_group(backend)
     else:
         torch.cuda.set_device(0)
+    prev_affinity = _bind_local_cpus(torch.cuda.current_device())
     import paper_1609_01010_b200 as mc
     from paper_1609_01010_b200 import _native, _tensors
 
@@ -311,6 +339,12 @@ def run_mine(args, cfg):
             mc.conv_batch(a, b, p, engine=engine, out=c)
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     torch.cuda.synchronize()
+    # clock sampling starts before the warm-up steps (its start-up pause must
+    # not sit between the warm-up and the timed steps: the first kernel after
+    # an idle GPU runs at half speed) and runs through the timed region
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    time.sleep(0.3)
 
     for _ in range(args.warmup):
         flush.zero_()
@@ -345,9 +379,6 @@ def run_mine(args, cfg):
         torch.cuda.synchronize()
 
     # ---- device-resident timed region: K steps, L2 flushed before each
-    clocks = ClockSampler(torch.cuda.current_device())
-    clocks.start()
-    time.sleep(0.3)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     launches0 = _native.launch_count()
@@ -363,6 +394,8 @@ def run_mine(args, cfg):
         launches = launches_per_step * args.steps
     clk = clocks.stop()
     times = [s.elapsed_time(e) for s, e in ev]  # ms
+    if os.environ.get("BENCH_STEP_TIMES"):
+        print("step times (ms):", " ".join(f"{t:.4f}" for t in times), file=sys.stderr)
     total_ms = sum(times)
     t_local = torch.tensor([total_ms], dtype=torch.float64, device=_coll_device(dev))
     if ws > 1:
@@ -454,6 +487,8 @@ def run_mine(args, cfg):
         bf, pw = 3 * full_count(L), L
     else:
         bf, pw = 3 * 3 * full_count(L), 3 * L
+    if prev_affinity:  # the CPU baseline uses every host thread again
+        os.sched_setaffinity(0, prev_affinity)
     cpu_rate, sample, cpu_cores = cpu_oracle_rate(cfg, host_threads(), target_s=args.ref_seconds)
     line = {
         "metric": "modular poly-mults/sec", "value": value, "unit": "products/s",
