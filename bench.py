@@ -373,6 +373,11 @@ def run_mine(args, cfg):
         def step():
             graph.replay()
 
+        for _ in range(args.warmup):  # the warm-up steps again, now as replays
+            flush.zero_()
+            step()
+        torch.cuda.synchronize()
+
     def barrier():
         if ws > 1:
             torch.distributed.barrier()
