@@ -26,7 +26,6 @@ import os
 import statistics
 import subprocess
 import sys
-import threading
 import time
 
 REPO = os.path.dirname(os.path.abspath(__file__))

@@ -17,7 +17,7 @@ from functools import lru_cache
 import torch
 
 from . import _native, _tensors
-from .field import FourierPrime, as_field, check_transform_size, root_of_unity
+from .field import as_field, check_transform_size, root_of_unity
 
 
 class OpCounters:
