@@ -39,6 +39,7 @@ struct FourParams {
     // twist tables [R][C] (row_conv_kernel<.., TT = true>): twf[r][x] =
     // w_L^(x * rev(r)), twi[r][x] = w_L^-(x * rev(r)) * L^-1 * 2^32, Shoup pairs
     const uint2 *twf, *twi;
+    int row_prefetch;  // L2 bulk prefetch of the next row (the row pass's data exceeds L2)
 };
 
 __device__ __forceinline__ u32 pow_w(const u32 *lo, const uint2 *hi, u32 e, u32 p) {
