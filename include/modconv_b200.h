@@ -60,6 +60,15 @@ mc_status mc_field_info(uint32_t p, int *two_adicity, uint32_t *generator);
 /* Principal 2^log2n-th root of unity (field.py:209-224 root_of_unity). */
 mc_status mc_root_of_unity(uint32_t p, int log2n, uint32_t *root);
 
+/* Select the primitive root g behind the roots of unity for p on the
+ * calling thread (g = 0: back to the smallest primitive root).  The
+ * reference's FourierPrime carries any valid generator
+ * (field.py:111-131), and TwiddleTable takes w_L = g^((p-1)/L) from it
+ * (transform.py:83, field.py:209-224); the transforms (mc_ntt, mc_tft,
+ * mc_itft) then match the reference for that generator.  Convolutions do
+ * not depend on the choice.  MC_EINVAL if g is not a primitive root mod p. */
+mc_status mc_use_generator(uint32_t p, uint32_t g);
+
 /* Build (or find cached) the twiddle tables for (device, p, log2L)
  * (transform.py:73-124 TwiddleTable/get_table).  Optional: every compute
  * call prepares what it needs; calling this up front keeps table

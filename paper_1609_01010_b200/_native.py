@@ -31,6 +31,7 @@ _SIGS = {
     "mc_field_info": ([u32, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(u32)], ctypes.c_int),
     "mc_root_of_unity": ([u32, ctypes.c_int, ctypes.POINTER(u32)], ctypes.c_int),
     "mc_field_prepare": ([u32, ctypes.c_int, ctypes.c_int], ctypes.c_int),
+    "mc_use_generator": ([u32, u32], ctypes.c_int),
     "mc_conv_fft_pad": ([vp, i64, i32, vp, i64, i32, vp, i64, i64, u32, vp], ctypes.c_int),
     "mc_conv_tft": ([vp, i64, i32, vp, i64, i32, vp, i64, i64, u32, vp], ctypes.c_int),
     "mc_circ_conv": ([vp, vp, vp, i32, i64, u32, vp], ctypes.c_int),

@@ -28,7 +28,7 @@ from dataclasses import dataclass, field as dc_field
 import torch
 
 from . import _native, _tensors
-from .field import FieldMismatchError, as_field, check_transform_size
+from .field import FieldMismatchError, FourierPrime, as_field, check_transform_size
 from .poly import DensePoly
 from .transform import OpCounters, full_count, itft_count, tft_count
 
@@ -117,6 +117,11 @@ def conv_batch(a: torch.Tensor, b: torch.Tensor, field, engine: str = "tft",
     defining sum, convolve.py:71-87; any length, no roots of unity) or
     "auto" (GpuPlanner).
     """
+    if stream is not None and stream != torch.cuda.current_stream():
+        # every temporary and the output are then allocated on `stream`, and
+        # the kernels run there: nothing is freed while `stream` still uses it
+        with torch.cuda.stream(stream):
+            return conv_batch(a, b, field, engine, out, counters, None)
     if engine not in ("tft", "fft_pad", "definition", "auto"):
         raise ValueError("batched engine must be 'tft', 'fft_pad', 'definition' or 'auto', "
                          f"got {engine!r}")
@@ -304,33 +309,47 @@ def _pow2_len(n: int, what: str = "length") -> int:
 
 
 def split_residues(u, p: int) -> tuple[list[int], list[int]]:
-    """Residues of u mod (x^n - 1) and mod (x^n + 1), n = len(u)/2
-    (convolve.py:214-219), on the GPU."""
+    """Residues of u mod (x^n - 1) and mod (x^n + 1), n = len(u) >> 1
+    (convolve.py:214-219), on the GPU.  Any length, like the reference: an
+    odd length's last coefficient takes no part; power-of-two lengths run the
+    fused kernel (mc_split_residues), others device tensor arithmetic."""
     size = len(u)
-    lg = _pow2_len(size) - 1 if size >= 2 else None
-    if lg is None:
-        raise ValueError("length must be a power of two >= 2")
+    n = size >> 1
     dev = _tensors.require_cuda()
+    if n == 0:
+        return [], []
     x = _tensors.list_to_device(u, p, dev)
-    a = torch.empty(size // 2, dtype=torch.int32, device=dev)
+    if size & (size - 1):
+        lo = x[:n].to(torch.int64)
+        hi = x[n:2 * n].to(torch.int64)
+        return (_tensors.device_to_list(((lo + hi) % p).to(torch.int32)),
+                _tensors.device_to_list(((lo - hi) % p).to(torch.int32)))
+    a = torch.empty(n, dtype=torch.int32, device=dev)
     b = torch.empty_like(a)
     _native.check(_native.lib().mc_split_residues(_tensors.ptr(x), _tensors.ptr(a),
-                                                  _tensors.ptr(b), lg, 1, p,
+                                                  _tensors.ptr(b), n.bit_length() - 1, 1, p,
                                                   _tensors.stream_handle()))
     return _tensors.device_to_list(a), _tensors.device_to_list(b)
 
 
 def recombine_residues(a, b, p: int) -> list[int]:
-    """Inverse of split_residues (convolve.py:222-227), on the GPU."""
-    if len(a) != len(b):
-        raise ValueError("residue halves must have equal lengths")
-    lg = _pow2_len(len(a))
+    """Inverse of split_residues (convolve.py:222-227), on the GPU: pairs
+    (a_j, b_j) up to the shorter length, like the reference's zip."""
+    n = min(len(a), len(b))
     dev = _tensors.require_cuda()
-    x = _tensors.list_to_device(a, p, dev)
-    y = _tensors.list_to_device(b, p, dev)
-    w = torch.empty(2 * len(a), dtype=torch.int32, device=dev)
+    if n == 0:
+        return []
+    x = _tensors.list_to_device(list(a[:n]), p, dev)
+    y = _tensors.list_to_device(list(b[:n]), p, dev)
+    if n & (n - 1):
+        inv2 = (p + 1) >> 1
+        xs, ys = x.to(torch.int64), y.to(torch.int64)
+        lo = (xs + ys) % p * inv2 % p
+        hi = (xs - ys) % p * inv2 % p
+        return _tensors.device_to_list(torch.cat([lo, hi]).to(torch.int32))
+    w = torch.empty(2 * n, dtype=torch.int32, device=dev)
     _native.check(_native.lib().mc_recombine_residues(_tensors.ptr(x), _tensors.ptr(y),
-                                                      _tensors.ptr(w), lg, 1, p,
+                                                      _tensors.ptr(w), n.bit_length() - 1, 1, p,
                                                       _tensors.stream_handle()))
     return _tensors.device_to_list(w)
 
@@ -402,8 +421,11 @@ def poly_mul(a, b, req: ConvRequest) -> DensePoly:
     if a.field.p != req.field.p:
         raise FieldMismatchError(f"request field {req.field.p} does not match operands {a.field.p}")
     fp = as_field(req.field)
+    # the result lives on the caller's field and class (convolve.py:277-278,
+    # 296): the reference's own DensePoly in, the reference's DensePoly out
+    cls = type(a) if hasattr(type(a), "zero") else DensePoly
     if not any(a.coeffs) or not any(b.coeffs):
-        return DensePoly.zero(fp)
+        return cls.zero(a.field)
     u = _trim(a.coeffs)
     v = _trim(b.coeffs)
     engine = _resolve_engine(len(u), len(v), req)
@@ -426,8 +448,11 @@ def poly_mul(a, b, req: ConvRequest) -> DensePoly:
         out = circ_conv_split(up, vp, req)[:out_len]
     else:
         raise ValueError(f"unknown engine {engine!r}")
-    # the engines return canonical residues: wrap without re-validating them
-    return DensePoly._trusted(fp, tuple(out)).normalize()
+    if cls is DensePoly:
+        # the engines return canonical residues: wrap without re-validating them
+        return DensePoly._trusted(a.field if isinstance(a.field, FourierPrime) else fp,
+                                  tuple(out)).normalize()
+    return cls(a.field, tuple(out)).normalize()
 
 
 def _trim(coeffs) -> list[int]:

@@ -40,6 +40,10 @@ def _dev_words(x, device) -> torch.Tensor:
 
 def mul_three_primes_tensor(a, b, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """Exact product limbs [3, n] (int32 bit patterns of uint32 limbs)."""
+    if stream is not None and stream != torch.cuda.current_stream():
+        # temporaries, scratch and the H2D copies then belong to `stream`
+        with torch.cuda.stream(stream):
+            return mul_three_primes_tensor(a, b, out, None)
     dev = _tensors.require_cuda()
     a_d = _dev_words(a, dev)
     b_d = _dev_words(b, dev)
@@ -72,6 +76,9 @@ def mul_three_primes(a, b) -> list[int]:
 def crt3(r1: torch.Tensor, r2: torch.Tensor, r3: torch.Tensor, out=None,
          stream=None) -> torch.Tensor:
     """Garner CRT of residue vectors mod PRIMES -> limbs [3, n]."""
+    if stream is not None and stream != torch.cuda.current_stream():
+        with torch.cuda.stream(stream):
+            return crt3(r1, r2, r3, out, None)
     r1, r2, r3 = (_tensors.as_words(r.reshape(-1)).contiguous() for r in (r1, r2, r3))
     n = r1.numel()
     if r2.numel() != n or r3.numel() != n:

@@ -5,6 +5,7 @@
 
 #include <cuda.h>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -504,7 +505,9 @@ mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t
                              const uint32_t *b, int64_t ldb, int32_t z2, uint32_t *c,
                              int64_t ldc, int64_t batch, uint32_t p, int64_t chunk_rows,
                              void *stream) {
-    static thread_local PipeState S;
+    // one pipeline state per (thread, device): streams, events and buffers
+    // belong to the device they were created on
+    static thread_local std::map<int, PipeState> states;
     if (engine != 0 && engine != 1) return fail(MC_EINVAL, "engine must be 0 (fft_pad) or 1 (tft)");
     if (z1 < 1 || z2 < 1) return fail(MC_EINVAL, "inputs must be nonempty");
     const int64_t n = (int64_t)z1 + z2 - 1;
@@ -534,6 +537,7 @@ mc_status mc_conv_host_async(int engine, const uint32_t *a, int64_t lda, int32_t
     // host reaches ~44 GB/s each way; kernel reads from host alongside any
     // host writes only ~36 (scripts/zc_probe{2,3,4}.py).
     const int dev = current_device();
+    PipeState &S = states[dev];
     if (S.dev != dev) {
         std::lock_guard<std::mutex> lock(g_pipe_mu);
         MC_CUDA_CHECK(cudaStreamCreateWithFlags(&S.s_in, cudaStreamNonBlocking));

@@ -164,13 +164,13 @@ struct TwistHost {
 };
 
 static std::mutex g_tw_mu;
-static std::map<std::tuple<int, u32, int>, TwistHost> g_tw;
+static std::map<std::tuple<int, u32, u32, int>, TwistHost> g_tw;  // (dev, p, w_L, K)
 
 static mc_status get_twist(const FieldTables *T, TwistTabs *out) {
     const int K = T->log2L;
     const u32 p = T->p;
     const int dev = current_device();
-    auto key = std::make_tuple(dev, p, K);
+    auto key = std::make_tuple(dev, p, T->root, K);
     std::lock_guard<std::mutex> lock(g_tw_mu);
     auto it = g_tw.find(key);
     if (it == g_tw.end()) {
@@ -235,7 +235,7 @@ __global__ void twist_table_kernel(TwistTabs tw, int KR, int KC, u32 p, Shoup sc
 struct FullTwist {
     uint2 *f = nullptr, *i = nullptr;
 };
-static std::map<std::tuple<int, u32, int, int>, FullTwist> g_full_tw;
+static std::map<std::tuple<int, u32, u32, int, int>, FullTwist> g_full_tw;
 
 static bool twist_table_on(int K) {
     static const int max_k = [] {
@@ -251,7 +251,7 @@ static mc_status get_full_twist(const FieldTables *T, const TwistTabs &tw, int K
                                 const uint2 **f, const uint2 **i) {
     const int K = T->log2L, KR = K - KC;
     const int dev = current_device();
-    auto key = std::make_tuple(dev, T->p, K, KC);
+    auto key = std::make_tuple(dev, T->p, T->root, K, KC);
     std::lock_guard<std::mutex> lock(g_tw_mu);
     auto it = g_full_tw.find(key);
     if (it == g_full_tw.end()) {
@@ -476,6 +476,8 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
         // cannot stay in the 126 MB L2 (config 4: -2.4%; config 5, 48 MB per
         // prime: +1.3% without this gate)
         P.row_prefetch = 8ll * L * P.chunk + 16ll * L > (96ll << 20) ? 1 : 0;
+        if (const char *f = getenv("MC_ROW_PREFETCH"))  // 0/1: force (sanitizer / A/B runs)
+            if (*f) P.row_prefetch = atoi(f) ? 1 : 0;
         cudaError_t e = launch_cols_any(KC, KR, NT, P, true, st, &tma);
         if (e == cudaSuccess) e = launch_rows_any(KC, KR, P, st);
         if (e == cudaSuccess) e = launch_cols_any(KC, KR, NT, P, false, st);

@@ -107,6 +107,29 @@ u32 smallest_primitive_root(u32 p) {
     }
 }
 
+static thread_local u32 g_gen_p = 0, g_gen_g = 0;
+
+u32 field_generator(u32 p) {
+    if (g_gen_p == p && g_gen_g) return g_gen_g;
+    static std::mutex mu;
+    static std::map<u32, u32> smallest;
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = smallest.find(p);
+    if (it == smallest.end()) it = smallest.emplace(p, smallest_primitive_root(p)).first;
+    return it->second;
+}
+
+static bool is_primitive_root(u32 g, u32 p) {
+    if (g < 2 || g >= p) return false;
+    u64 m = p - 1;
+    for (u64 q = 2; q * q <= m; ++q) {
+        if (m % q) continue;
+        if (powmod(g, (p - 1) / q, p) == 1) return false;
+        while (m % q == 0) m /= q;
+    }
+    return m == 1 || powmod(g, (p - 1) / m, p) != 1;
+}
+
 Shoup shoup(u32 w, u32 p) {
     Shoup s;
     s.w = w;
@@ -135,7 +158,7 @@ mc_status check_field(u32 p, int log2L) {
 
 // ----------------------------------------------------------------- tables
 static std::mutex g_tab_mu;
-static std::map<std::tuple<int, u32, int>, FieldTables *> g_tabs;
+static std::map<std::tuple<int, u32, u32, int>, FieldTables *> g_tabs;
 
 int current_device() {
     int d = 0;
@@ -176,7 +199,8 @@ mc_status get_tables(u32 p, int log2L, const FieldTables **out) {
     mc_status st = check_field(p, log2L);
     if (st != MC_OK) return st;
     int dev = current_device();
-    auto key = std::make_tuple(dev, p, log2L);
+    const u32 g = field_generator(p);
+    auto key = std::make_tuple(dev, p, g, log2L);
     std::lock_guard<std::mutex> lock(g_tab_mu);
     auto it = g_tabs.find(key);
     if (it != g_tabs.end()) {
@@ -187,7 +211,7 @@ mc_status get_tables(u32 p, int log2L, const FieldTables **out) {
     const u64 L = 1ull << log2L;
     T->p = p;
     T->log2L = log2L;
-    u32 g = smallest_primitive_root(p);
+    T->gen = g;
     T->root = (u32)powmod(g, (p - 1) >> log2L, p);
     // Montgomery inverse p^-1 mod 2^32 (Newton iteration)
     u32 inv = p;
@@ -274,8 +298,23 @@ mc_status mc_root_of_unity(uint32_t p, int log2n, uint32_t *root) {
                             std::to_string(log2n) + ", field p=" + std::to_string(p) +
                             " has " + std::to_string(a),
                         log2n);
-    uint32_t g = mc::smallest_primitive_root(p);
+    uint32_t g = mc::field_generator(p);
     if (root) *root = (uint32_t)mc::powmod(g, (uint64_t)(p - 1) >> log2n, p);
+    return MC_OK;
+}
+
+mc_status mc_use_generator(uint32_t p, uint32_t g) {
+    if (g == 0) {
+        if (mc::g_gen_p == p) mc::g_gen_p = mc::g_gen_g = 0;
+        return MC_OK;
+    }
+    if (p < 3 || !(p & 1) || !mc::is_prime_u32(p))
+        return mc::fail(MC_EINVAL, "modulus must be an odd prime: " + std::to_string(p));
+    if (!mc::is_primitive_root(g, p))
+        return mc::fail(MC_EINVAL, std::to_string(g) + " is not a primitive root mod " +
+                                       std::to_string(p));
+    mc::g_gen_p = p;
+    mc::g_gen_g = g;
     return MC_OK;
 }
 

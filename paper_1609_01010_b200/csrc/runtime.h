@@ -29,6 +29,9 @@ u64 powmod(u64 b, u64 e, u64 p);
 bool is_prime_u32(u64 n);
 int two_adicity(u64 p);
 u32 smallest_primitive_root(u32 p);
+// Generator behind the roots of unity for p on this thread: the one set by
+// mc_use_generator(p, g), else the smallest primitive root (field.py:102-108).
+u32 field_generator(u32 p);
 Shoup shoup(u32 w, u32 p);
 u32 inv_mod(u32 a, u32 p);
 
@@ -43,7 +46,8 @@ mc_status check_field(u32 p, int log2L);
 struct FieldTables {
     u32 p = 0;
     int log2L = 0;
-    u32 root = 0;       // w_L (field.py:209-224)
+    u32 gen = 0;        // primitive root the tables are built from
+    u32 root = 0;       // w_L = gen^((p-1)/L) (field.py:209-224)
     u32 pinv = 0;       // p^-1 mod 2^32 (Montgomery)
     Shoup linv;         // L^-1 mod p
     Shoup linv_mont;    // L^-1 * 2^32 mod p (undoes REDC's 2^-32)

@@ -17,7 +17,7 @@ from functools import lru_cache
 import torch
 
 from . import _native, _tensors
-from .field import as_field, check_transform_size, root_of_unity
+from .field import as_field, check_transform_size, root_of_unity, smallest_generator
 
 
 class OpCounters:
@@ -102,7 +102,8 @@ class TwiddleTable:
         self.inv_size = pow(size, fp.p - 2, fp.p)
         self._powers = None
         if torch.cuda.is_available():
-            _native.check(_native.lib().mc_field_prepare(fp.p, log2, -1))
+            with _generator(fp):
+                _native.check(_native.lib().mc_field_prepare(fp.p, log2, -1))
 
     @property
     def powers(self) -> list[int]:
@@ -120,14 +121,35 @@ class TwiddleTable:
         return [1] + pw[:0:-1]
 
 
-_TABLE_CACHE: dict[tuple[int, int], TwiddleTable] = {}
+_TABLE_CACHE: dict[tuple[int, int, int], TwiddleTable] = {}
 _TABLE_LOCK = threading.Lock()
 
 
+class _generator:
+    """Run the native transforms with the field's own generator (thread-local
+    selection in the library, mc_use_generator) when it is not the smallest
+    primitive root -- the reference builds every table from field.generator
+    (transform.py:83)."""
+
+    __slots__ = ("p", "g")
+
+    def __init__(self, fp):
+        self.p = fp.p
+        self.g = fp.generator if fp.generator != smallest_generator(fp.p) else 0
+
+    def __enter__(self):
+        if self.g:
+            _native.check(_native.lib().mc_use_generator(self.p, self.g))
+
+    def __exit__(self, *exc):
+        if self.g:
+            _native.lib().mc_use_generator(self.p, 0)
+
+
 def get_table(field, size: int) -> TwiddleTable:
-    """Shared table for (p, size); built once (transform.py:110-124)."""
+    """Shared table for (p, generator, size); built once (transform.py:110-124)."""
     fp = as_field(field)
-    key = (fp.p, size)
+    key = (fp.p, fp.generator, size)
     t = _TABLE_CACHE.get(key)
     if t is None:
         with _TABLE_LOCK:
@@ -150,8 +172,9 @@ def moddft(x, table: TwiddleTable, direction: str = "fwd", counters: OpCounters 
     p = table.field.p
     xt = _tensors.list_to_device(x, p, dev)
     y = torch.empty_like(xt)
-    _native.check(_native.lib().mc_ntt(_tensors.ptr(xt), _tensors.ptr(y), table.log2_size, 1, p,
-                                       int(direction == "inv"), _tensors.stream_handle()))
+    with _generator(table.field):
+        _native.check(_native.lib().mc_ntt(_tensors.ptr(xt), _tensors.ptr(y), table.log2_size, 1,
+                                           p, int(direction == "inv"), _tensors.stream_handle()))
     if counters is not None:
         counters.butterflies += full_count(n)
     return _tensors.device_to_list(y)
@@ -225,8 +248,9 @@ def tft(table: TwiddleTable, x, n: int, counters: OpCounters | None = None):
     p = table.field.p
     xt = _tensors.list_to_device(x, p, dev)
     y = torch.empty(n, dtype=torch.int32, device=dev)
-    _native.check(_native.lib().mc_tft(_tensors.ptr(xt), z, _tensors.ptr(y), n, table.log2_size,
-                                       1, p, _tensors.stream_handle()))
+    with _generator(table.field):
+        _native.check(_native.lib().mc_tft(_tensors.ptr(xt), z, _tensors.ptr(y), n,
+                                           table.log2_size, 1, p, _tensors.stream_handle()))
     if counters is not None:
         counters.butterflies += tft_count(size, z, n)
     return _tensors.device_to_list(y)
@@ -245,8 +269,9 @@ def itft(table: TwiddleTable, xhat, counters: OpCounters | None = None):
     p = table.field.p
     xt = _tensors.list_to_device(xhat, p, dev)
     y = torch.empty(n, dtype=torch.int32, device=dev)
-    _native.check(_native.lib().mc_itft(_tensors.ptr(xt), _tensors.ptr(y), n, table.log2_size, 1,
-                                        p, _tensors.stream_handle()))
+    with _generator(table.field):
+        _native.check(_native.lib().mc_itft(_tensors.ptr(xt), _tensors.ptr(y), n,
+                                            table.log2_size, 1, p, _tensors.stream_handle()))
     if counters is not None:
         counters.butterflies += itft_count(size, n)
     return _tensors.device_to_list(y)

@@ -4,6 +4,7 @@ Run in the build container (where /root/reference exists):
 
     python tests/golden/make_golden.py            # small fixtures (seconds)
     python tests/golden/make_golden.py --cfg5     # + config-5 pin (~2 min)
+    python tests/golden/make_golden.py --cfg4     # + config-4 pin (rows 0 and 7, ~8 min)
 
 It imports the unmodified reference package `modconv` from
 /root/reference/pkg/src and records its outputs for seeded inputs built with
@@ -278,6 +279,8 @@ def cfg5_pin():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg5", action="store_true", help="also pin config 5 (~2 min)")
+    ap.add_argument("--cfg4", action="store_true",
+                    help="also pin config 4 rows 0 and 7 (~4 min per row)")
     args = ap.parse_args()
     rng = random.Random(0x1609_01010)
     small = {
@@ -302,14 +305,17 @@ def main():
             config_row(3, P2, 4096, 4096, 3, [0, 65535], "fft_pad"),
         ],
     }
+    old = os.path.join(HERE, "reference_configs.json")
+    prev = json.load(open(old)) if os.path.exists(old) else {}
     if args.cfg5:
         cfgs["cfg5"] = cfg5_pin()
-    else:
-        old = os.path.join(HERE, "reference_configs.json")
-        if os.path.exists(old):
-            prev = json.load(open(old))
-            if "cfg5" in prev:
-                cfgs["cfg5"] = prev["cfg5"]
+    elif "cfg5" in prev:
+        cfgs["cfg5"] = prev["cfg5"]
+    if args.cfg4:
+        # one reference poly_mul at L = 2^23 takes ~4 min and ~3 GB
+        cfgs["cfg4"] = config_row(4, P3, 1 << 22, 1 << 22, 4, [0, 7], "fft_pad")
+    elif "cfg4" in prev:
+        cfgs["cfg4"] = prev["cfg4"]
     with open(os.path.join(HERE, "reference_configs.json"), "w") as f:
         json.dump(cfgs, f, indent=1)
     print("wrote", os.listdir(HERE))

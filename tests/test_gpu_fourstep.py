@@ -54,15 +54,22 @@ def test_fourstep_circular(orc, K):
     assert got == fold.tolist()
 
 
-def test_cfg4_large_products(orc):
+def test_cfg4_large_products(orc, golden_configs):
     """Config 4: 8 products of 2^22 x 2^22 mod 2013265921 (L = 2^23).
-    Products 0 and 7 bit-exact vs the oracle; all 8 pass the evaluation
-    identity at two points."""
+    Products 0 and 7 equal the reference's own poly_mul (sha256 pins made by
+    tests/golden/make_golden.py --cfg4) and the oracle; all 8 pass the
+    evaluation identity at two points."""
     p, z, B = P3, 1 << 22, 8
     a = gen_device(4, 0, 0, B, z, p)
     b = gen_device(4, 1, 0, B, z, p)
     c = mc.conv_batch(a, b, p, engine="fft_pad")
     torch.cuda.synchronize()
+    pin = golden_configs["cfg4"]
+    assert (pin["p"], pin["z1"], pin["z2"], pin["seed"]) == (p, z, z, 4)
+    for rec in pin["rows"]:
+        row = to_u32_np(c[rec["row"]])
+        assert hashlib.sha256(row.tobytes()).hexdigest() == rec["sha256"], rec["row"]
+        assert row[:8].tolist() == rec["head"] and row[-8:].tolist() == rec["tail"]
     for r in (0, B - 1):
         want, _, _ = orc.conv_batch(to_u32_np(a[r:r + 1]), to_u32_np(b[r:r + 1]), p)
         assert np.array_equal(to_u32_np(c[r:r + 1]), want), r

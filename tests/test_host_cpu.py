@@ -186,3 +186,75 @@ def test_kernel_model_matches_oracle(orc):
             v = [rng.randrange(p) for _ in range(z2)]
             got, _ = km.conv_tft_model(u, v, p, lambda L: orc.root_of_unity(p, L.bit_length() - 1))
             assert got == orc.schoolbook(u, v, p), (p, z1, z2)
+
+
+def test_factorization_large_safe_prime_is_fast():
+    """Primitive roots come from a rho factorization (field.py:61-95): a
+    62-bit safe prime's descriptor is built at once (trial division of p-1
+    would take ~2^30 steps)."""
+    import time
+
+    from paper_1609_01010_b200.field import factorize
+
+    t0 = time.perf_counter()
+    fp = mc.FourierPrime.from_modulus(2305843009213699919)
+    assert time.perf_counter() - t0 < 1.0
+    assert (fp.two_adicity, fp.generator) == (1, 13)
+    assert factorize(2305843009213699918) == (2, 1152921504606849959)
+    assert factorize(1) == ()
+    assert factorize(2**4 * 3**3 * 1000003 * 998244353) == (2, 3, 1000003, 998244353)
+    assert factorize((2**31 - 1) * (2**31 - 19)) == (2**31 - 19, 2**31 - 1)
+
+
+def test_large_field_rejected_before_any_work():
+    """conv_batch on a field the 32-bit kernels cannot host raises
+    UnsupportedSizeError at once (no hang, no device needed)."""
+    import torch
+
+    fp = mc.FourierPrime.from_modulus(2305843009213699919)
+    one = torch.ones((1, 1), dtype=torch.int32)
+    with pytest.raises(mc.UnsupportedSizeError):
+        mc.conv_batch(one, one, fp, engine="fft_pad")
+    with pytest.raises(mc.UnsupportedSizeError) as e:
+        mc.conv_batch(torch.ones((1, 3), dtype=torch.int32), one.repeat(1, 2), fp)
+    assert e.value.required_two_adicity == 2
+
+
+def test_felt_constructors():
+    """FourierPrime.felt / zero / one (field.py:140-150)."""
+    fp = mc.FourierPrime.from_modulus(P3)
+    assert fp.felt(-1).value == P3 - 1
+    assert fp.felt(P3 + 5).value == 5
+    assert fp.zero().value == 0 and fp.one().value == 1
+    assert (fp.one() + fp.felt(-1)) == fp.zero()
+
+
+def test_foreign_field_keeps_its_generator():
+    """A duck-typed field (the reference's FourierPrime) keeps its generator:
+    FourierPrime(17, 4, 5) has w_16 = 5, not the smallest root's 3."""
+
+    class Foreign:
+        p, two_adicity, generator = 17, 4, 5
+
+    from paper_1609_01010_b200.field import as_field
+
+    fp = as_field(Foreign())
+    assert fp.generator == 5
+    assert mc.root_of_unity(fp, 16).value == 5
+    assert mc.root_of_unity(as_field(17), 16).value == 3
+    with pytest.raises(ValueError):
+        class Bad:
+            p, two_adicity, generator = 17, 4, 4
+
+        as_field(Bad())
+
+
+def test_use_generator_validates():
+    lib = _native.lib()
+    assert lib.mc_use_generator(17, 4) == _native.MC_EINVAL  # order 4, not primitive
+    assert lib.mc_use_generator(15, 2) == _native.MC_EINVAL
+    assert lib.mc_use_generator(17, 5) == 0
+    r = ctypes.c_uint32()
+    assert lib.mc_root_of_unity(17, 4, ctypes.byref(r)) == 0 and r.value == 5
+    assert lib.mc_use_generator(17, 0) == 0
+    assert lib.mc_root_of_unity(17, 4, ctypes.byref(r)) == 0 and r.value == 3
