@@ -1,21 +1,33 @@
 """Benchmark of the modular polynomial-multiplication hot path on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--config 1..5]
-                    [--impl mine|reference]
+                    [--configs 1,2,3,4,5] [--impl mine|reference] [--plan-only]
 
-Default workload = BASELINE.json configs[1] (config 2): a batch of 4096
-products of seeded uniform residues mod p = 2013265921, operand lengths
-1500 x 2100 -> 3599 coefficients, truncated-transform engine (conv_tft) at
-L = 4096.  One step = one batched call over the whole batch.  Under
-torchrun each rank multiplies its own 4096-product shard of the seeded stream
-(weak scaling, no collective on the data path); value = all ranks' products
-/ max-over-ranks device time.
+Headline (`value`) = BASELINE.json configs[1] (config 2): 4096 products of
+seeded uniform residues mod p = 2013265921, operand lengths 1500 x 2100 ->
+3599 coefficients, truncated-transform engine (conv_tft) at L = 4096.  One
+step = one batched call over the whole batch.  The same run times every
+other BASELINE config the same way (device-resident inputs, L2 flushed
+before every timed step, CUDA events on the launching stream, pinned-host
+e2e through the public API, CPU baseline) and reports them under
+`all_configs`.
 
-Reported: products/s (metric), Gcoeff/s (output coefficients), the HBM
-roofline of the fused kernel (algorithmic bytes 4*(z1+z2+n) per product),
-the integer-pipe view (butterflies/s), the end-to-end number through the
-public API with host (pinned) buffers, and the CPU baseline = the C oracle
-port of the reference path timed on this host's cores.
+Multi-GPU: `--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run (N ranks, 127.0.0.1), one process per GPU over NCCL.
+Each config's global batch is partitioned over the ranks (strong scaling,
+distributed.shard_rows): config 2 4096/N, config 3 65536/N, config 4 8/N;
+config 1 (one product) runs as replicas; config 5 spreads the three primes
+over the ranks and fuses the residue gather into the CRT kernel over peer
+memory.  Time = max over ranks of the CUDA-event time between barriers;
+value = the config's global products / that time.
+
+Reported per config: products/s, Gcoeff/s (output coefficients), the HBM
+roofline (compulsory bytes 4*(z1+z2+n) per product for the fused kernel,
+the four-step pass model 4*(z1+z2+n+6L) for configs 4-5), the integer-pipe
+view against the nominal 16 butterflies/clk/SM and the measured practical
+ceiling, the end-to-end rate through the public API with pinned host
+buffers, and the CPU baseline = the C oracle port of the reference path on
+this host's cores.
 """
 
 from __future__ import annotations
@@ -23,6 +35,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -45,6 +58,8 @@ CONFIGS = {
     5: dict(name="cfg5_three_primes_2^20x2^20_crt", p=0, z1=1 << 20, z2=1 << 20, batch=1,
             engine="three_primes", seed=5),
 }
+HEADLINE = 2
+METRIC = "modular poly-mults/sec"
 
 L2_FLUSH_BYTES = 256 << 20  # > 126 MB L2
 
@@ -218,7 +233,10 @@ def cpu_oracle_rate(cfg, threads: int, target_s: float = 10.0, max_products=None
     b = oracle.gen_u32(cfg["seed"], 1, 0, cal, z2, p)
     t0 = time.perf_counter()
     oracle.conv_batch(a, b, p, engine, threads=threads)
-    per = (time.perf_counter() - t0) / cal
+    dt = time.perf_counter() - t0
+    per = dt / cal
+    if dt >= 0.5 * target_s or cal == B:  # the calibration slice is the sample
+        return cal / dt, f"{cal} of {B} products (rows 0..{cal - 1}), {threads} threads", threads
     nsamp = int(min(B, max(cal, target_s / max(per, 1e-9))))
     if max_products:
         nsamp = min(nsamp, max_products)
@@ -237,123 +255,210 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def run_reference(args, cfg):
-    """--impl reference: the reference path's CPU implementation (the C
-    oracle port; the reference itself is pure Python and does not travel to
-    the GPU box) with all host threads, same config/metric."""
-    ws, rank, _ = _dist()
-    if rank != 0:
-        return
-    from oracle import oracle
 
-    oracle.lib()
-    threads = host_threads()
+
+# ----------------------------------------------------------------- workload
+def config_dict(cfg) -> dict:
+    """The workload, identical in both arms (and at every N)."""
     n = cfg["z1"] + cfg["z2"] - 1
-    rates = []
-    sample = None
-    for i in range(args.warmup + args.steps):
-        r, sample, used = cpu_oracle_rate(cfg, threads, target_s=args.ref_step_seconds)
-        if i >= args.warmup:
-            rates.append(r)
-    v = statistics.median(rates)
-    line = {
-        "impl": "reference", "metric": "modular poly-mults/sec", "value": v,
-        "unit": "products/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * cfg["batch"] / v, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded splitmix64)",
-        "config": {"workload": cfg["name"], "batch": cfg["batch"], "z1": cfg["z1"],
-                   "z2": cfg["z2"], "n": n, "p": cfg["p"], "engine": cfg["engine"]},
-        "gcoeff_per_s": v * n / 1e9,
-        "cpu_baseline": {"value": v, "unit": "products/s", "cores": used, "kind": "port",
-                         "sample": sample + " per step; C restatement of the reference "
-                                            "(oracle/modconv_oracle.c)"},
-        "e2e": {"value": v, "unit": "products/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-    }
-    print(json.dumps(line), flush=True)
+    d = {"workload": cfg["name"], "global_batch": cfg["batch"], "z1": cfg["z1"],
+         "z2": cfg["z2"], "n": n, "L": 1 << (n - 1).bit_length(), "engine": cfg["engine"]}
+    if cfg["engine"] == "three_primes":
+        d["p"] = [P1, P2, P3]
+        d["input_bound"] = 1 << 30
+    else:
+        d["p"] = cfg["p"]
+    return d
 
 
-def run_mine(args, cfg):
+def partition(cfg, ws: int, rank: int) -> tuple[int, int, str]:
+    """(row0, rows, mode) of this rank's share of the config's global batch.
+
+    shards   -- contiguous rows of the batch (distributed.shard_rows): strong
+                scaling, no collective on the data path;
+    replicas -- a single product (config 1): every rank multiplies its own
+                copy (replicas only; value counts every rank's product);
+    primes   -- config 5: one product, its three primes spread over ranks."""
+    from paper_1609_01010_b200.distributed import shard_rows
+
+    if cfg["engine"] == "three_primes":
+        return 0, 1, "primes"
+    if cfg["batch"] == 1:
+        return 0, 1, "replicas"
+    row0, rows = shard_rows(cfg["batch"], ws, rank)
+    return row0, rows, "shards"
+
+
+def global_products(cfg, ws: int, mode: str) -> int:
+    return ws if mode == "replicas" else cfg["batch"]
+
+
+def bytes_model(cfg) -> tuple[int, str]:
+    """Algorithmic bytes per step over the whole global batch."""
+    z1, z2, B = cfg["z1"], cfg["z2"], cfg["batch"]
+    n = z1 + z2 - 1
+    L = 1 << (n - 1).bit_length()
+    if cfg["engine"] == "three_primes":
+        return (4 * (z1 + z2) + 12 * n + 3 * 4 * 6 * L,
+                "4*(z1+z2) in + 12*n limbs out + 3 primes x 4*6L four-step passes")
+    if L > 8192:
+        return 4 * (z1 + z2 + n + 6 * L) * B, "four-step pass model 4*(z1+z2+n+6L) per product"
+    return 4 * (z1 + z2 + n) * B, "compulsory 4*(z1+z2+n) per product (fused single pass)"
+
+
+def butterflies(cfg) -> tuple[int, int]:
+    """Reference OpCounters per product (butterflies, pointwise products)."""
+    from paper_1609_01010_b200.transform import full_count, itft_count, tft_count
+
+    n = cfg["z1"] + cfg["z2"] - 1
+    L = 1 << (n - 1).bit_length()
+    if cfg["engine"] == "tft":
+        return (tft_count(L, cfg["z1"], n) + tft_count(L, cfg["z2"], n) + itft_count(L, n), n)
+    if cfg["engine"] == "fft_pad":
+        return 3 * full_count(L), L
+    return 3 * 3 * full_count(L), 3 * L
+
+
+# ----------------------------------------------------------------- launcher
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def relaunch(args) -> int:
+    """--gpus N outside torchrun: run this script under torch.distributed.run
+    with N ranks on this node (one process per GPU), rendezvous on
+    127.0.0.1.  Returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def init_dist(ws: int, local: int, gpu: bool):
+    if ws <= 1:
+        return
     import torch
+    import torch.distributed as dist
 
+    # BENCH_BACKEND=gloo: host-side collectives only (CPU tests, --plan-only)
+    backend = os.environ.get("BENCH_BACKEND", "nccl" if gpu else "gloo")
+    if backend == "nccl":
+        torch.cuda.set_device(local % torch.cuda.device_count())
+        dist.init_process_group("nccl", device_id=torch.device("cuda", torch.cuda.current_device()))
+    else:
+        if gpu:
+            torch.cuda.set_device(local % torch.cuda.device_count())
+        dist.init_process_group("gloo")
+
+
+def _allreduce(vals: list, op: str, dev) -> list:
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()):
+        return vals
+    t = torch.tensor(vals, dtype=torch.float64, device=_coll_device(dev))
+    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+def plan_only(args, cfg_ids) -> None:
+    """--plan-only: the multi-rank plumbing without kernels (runs on CPU):
+    rank count, every rank's partition of each config, and the sum of the
+    shards, which must equal each config's global batch."""
     ws, rank, local = _dist()
+    init_dist(ws, local, gpu=False)
+    out = {}
+    for c in cfg_ids:
+        cfg = CONFIGS[c]
+        row0, rows, mode = partition(cfg, ws, rank)
+        ranges = [[row0, rows]]
+        if ws > 1:
+            import torch.distributed as dist
+
+            allr = [None] * ws
+            dist.all_gather_object(allr, [row0, rows], group=None)
+            ranges = allr
+        covered = sum(r[1] for r in ranges) if mode == "shards" else cfg["batch"]
+        out[f"cfg{c}"] = {"mode": mode, "ranges": ranges, "covered_rows": covered,
+                          "global_products": global_products(cfg, ws, mode),
+                          "config": config_dict(cfg)}
+    if rank == 0:
+        print(json.dumps({"plan_only": True, "n_gpus": ws, "configs": out}), flush=True)
     if ws > 1:
         import torch.distributed as dist
 
-        # BENCH_BACKEND=gloo exercises the multi-rank path on a single GPU
-        # (host-side barriers / reductions only; no rank waits on another's
-        # kernels).  Production runs use NCCL, one GPU per rank.
-        backend = os.environ.get("BENCH_BACKEND", "nccl")
-        ngpu = torch.cuda.device_count()
-        torch.cuda.set_device(local % ngpu)
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    else:
-        torch.cuda.set_device(0)
-    prev_affinity = _bind_local_cpus(torch.cuda.current_device())
+        dist.destroy_process_group()
+
+
+# ----------------------------------------------------------------- GPU arm
+def measure(cfg, args, ws: int, rank: int) -> dict:
+    """Device-resident timed steps, then the pinned-host e2e steps, of one
+    config on this rank's partition.  Returns the config's record (rank 0's
+    copy carries the max-over-ranks times)."""
+    import torch
+
     import paper_1609_01010_b200 as mc
     from paper_1609_01010_b200 import _native, _tensors
 
     lib = _native.lib()
     dev = torch.device("cuda", torch.cuda.current_device())
-    p, z1, z2, B = cfg["p"], cfg["z1"], cfg["z2"], cfg["batch"]
+    p, z1, z2 = cfg["p"], cfg["z1"], cfg["z2"]
     n = z1 + z2 - 1
-    L = 1 << (n - 1).bit_length()
     engine = cfg["engine"]
+    row0, rows, mode = partition(cfg, ws, rank)
     stream = torch.cuda.current_stream()
     sh = _tensors.stream_handle()
-
-    # inputs: this rank's shard of the seeded stream, resident in HBM
-    a = torch.empty((B, z1), dtype=torch.int32, device=dev)
-    b = torch.empty((B, z2), dtype=torch.int32, device=dev)
-    row0 = 0 if engine == "three_primes" else rank * B
     hi = p if engine != "three_primes" else (1 << 30)
-    _native.check(lib.mc_gen_u32(cfg["seed"], 0, row0, B, z1, hi, a.data_ptr(), z1, sh))
-    _native.check(lib.mc_gen_u32(cfg["seed"], 1, row0, B, z2, hi, b.data_ptr(), z2, sh))
-    if engine == "three_primes" and ws > 1:
-        # one product, primes spread over the ranks; the residues meet in the
-        # CRT: by default each rank's Garner slice reads them from the GPUs
-        # that computed them and writes rank 0's limbs over peer memory (the
-        # gather fused into the kernel); MC_CRT_NCCL=1 gathers them to rank 0
-        # with NCCL send/recv first
-        from paper_1609_01010_b200.distributed import (mul_three_primes_distributed,
-                                                       mul_three_primes_p2p)
 
+    a = torch.empty((max(rows, 1), z1), dtype=torch.int32, device=dev)
+    b = torch.empty((max(rows, 1), z2), dtype=torch.int32, device=dev)
+    if rows:
+        _native.check(lib.mc_gen_u32(cfg["seed"], 0, row0, rows, z1, hi, a.data_ptr(), z1, sh))
+        _native.check(lib.mc_gen_u32(cfg["seed"], 1, row0, rows, z2, hi, b.data_ptr(), z2, sh))
+    a, b = a[:rows], b[:rows]
+    if engine == "three_primes":
         c = torch.empty((3, n), dtype=torch.int32, device=dev)
-        dist_fn = mul_three_primes_distributed if os.environ.get("MC_CRT_NCCL") else mul_three_primes_p2p
+        if ws > 1:
+            from paper_1609_01010_b200.distributed import mul_three_primes_p2p
 
-        def step():
-            dist_fn(a[0], b[0], dst=0)
-    elif engine == "three_primes":
-        c = torch.empty((3, n), dtype=torch.int32, device=dev)
-
-        def step():
-            mc.mul_three_primes_tensor(a[0], b[0], out=c)
+            def step(x=a[0], y=b[0]):
+                r = mul_three_primes_p2p(x, y, dst=0)
+                if r is not None:
+                    c.copy_(r)
+        else:
+            def step(x=a[0], y=b[0]):
+                mc.mul_three_primes_tensor(x, y, out=c)
     else:
-        c = torch.empty((B, n), dtype=torch.int32, device=dev)
+        c = torch.empty((rows, n), dtype=torch.int32, device=dev)
 
-        def step():
-            mc.conv_batch(a, b, p, engine=engine, out=c)
+        def step(x=a, y=b):
+            if rows:
+                mc.conv_batch(x, y, p, engine=engine, out=c)
+
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
     torch.cuda.synchronize()
-    # clock sampling starts before the warm-up steps (its start-up pause must
-    # not sit between the warm-up and the timed steps: the first kernel after
-    # an idle GPU runs at half speed) and runs through the timed region
+    # clock sampling starts before the warm-up (its start-up pause must not
+    # sit between the warm-up and the timed steps) and runs through the
+    # timed region
     clocks = ClockSampler(torch.cuda.current_device())
     clocks.start()
     time.sleep(0.3)
-
     for _ in range(args.warmup):
         flush.zero_()
         step()
     torch.cuda.synchronize()
     graph = None
-    if (B * n <= (1 << 20) and engine != "three_primes") or (engine == "three_primes" and ws == 1):
-        # launch-bound workloads (config 1; config 5's ~20 launches and stream-
-        # ordered allocations per step): replay the step from a CUDA graph so
-        # the timed region measures the device, not the Python launch path
+    launches_per_step = None
+    if rows and ((rows * n <= (1 << 20) and engine != "three_primes")
+                 or (engine == "three_primes" and ws == 1)):
+        # launch-bound workloads (config 1; config 5's launches and stream-
+        # ordered allocations): replay the step from a CUDA graph so the timed
+        # region measures the device, not the Python launch path
         l0 = _native.launch_count()
         step()
         launches_per_step = _native.launch_count() - l0
@@ -367,12 +472,11 @@ def run_mine(args, cfg):
         torch.cuda.synchronize()
         assert torch.equal(c, eager_out), "graph replay differs from the eager step"
         del eager_out
-        step_eager = step
 
         def step():
             graph.replay()
 
-        for _ in range(args.warmup):  # the warm-up steps again, now as replays
+        for _ in range(args.warmup):  # the warm-up again, now as replays
             flush.zero_()
             step()
         torch.cuda.synchronize()
@@ -382,7 +486,6 @@ def run_mine(args, cfg):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
-    # ---- device-resident timed region: K steps, L2 flushed before each
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     launches0 = _native.launch_count()
@@ -399,128 +502,197 @@ def run_mine(args, cfg):
     clk = clocks.stop()
     times = [s.elapsed_time(e) for s, e in ev]  # ms
     if os.environ.get("BENCH_STEP_TIMES"):
-        print("step times (ms):", " ".join(f"{t:.4f}" for t in times), file=sys.stderr)
-    total_ms = sum(times)
-    t_local = torch.tensor([total_ms], dtype=torch.float64, device=_coll_device(dev))
-    if ws > 1:
-        torch.distributed.all_reduce(t_local, op=torch.distributed.ReduceOp.MAX)
-    t_max = float(t_local.item())
-    strong = engine == "three_primes" and ws > 1  # one product shared by all ranks
-    products = B * args.steps * (1 if strong else ws)
-    value = products / (t_max / 1e3)
-    ms_step = t_max / args.steps
+        print(cfg["name"], "step times (ms):", " ".join(f"{t:.4f}" for t in times),
+              file=sys.stderr)
+    t_max = _allreduce([sum(times)], "max", dev)[0]
+    launches_all, rows_all = _allreduce([float(launches), float(rows)], "sum", dev)
+    products = global_products(cfg, ws, mode)
+    value = products * args.steps / (t_max / 1e3)
 
     # ---- end to end through the public API with pinned host buffers
-    e2e = None
     if engine != "three_primes":
         a_h = a.cpu().pin_memory()
         b_h = b.cpu().pin_memory()
-        c_h = torch.empty((B, n), dtype=torch.int32).pin_memory()
-        for _ in range(max(1, args.warmup)):
-            mc.conv_batch(a_h, b_h, p, engine=engine, out=c_h)
-        torch.cuda.synchronize()
-        ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-        barrier()
-        for i in range(args.steps):
-            flush.zero_()
-            ev2[i][0].record(stream)
-            mc.conv_batch(a_h, b_h, p, engine=engine, out=c_h)
-            ev2[i][1].record(stream)
-        barrier()
-        t2 = torch.tensor([sum(s.elapsed_time(e) for s, e in ev2)], dtype=torch.float64,
-                          device=_coll_device(dev))
-        if ws > 1:
-            torch.distributed.all_reduce(t2, op=torch.distributed.ReduceOp.MAX)
-        assert torch.equal(c_h.to(dev), c), "e2e output differs from device-resident output"
-        e2e = {"value": products / (float(t2.item()) / 1e3), "unit": "products/s",
-               "h2d_bytes_per_step": 4 * B * (z1 + z2), "d2h_bytes_per_step": 4 * B * n}
+        c_h = torch.empty((rows, n), dtype=torch.int32).pin_memory()
+
+        def e2e_step():
+            if rows:
+                mc.conv_batch(a_h, b_h, p, engine=engine, out=c_h)
+        h2d, d2h = 4 * cfg["batch"] * (z1 + z2), 4 * cfg["batch"] * n
+        if mode == "replicas":
+            h2d, d2h = h2d * ws, d2h * ws
     else:
         a_h = a[0].cpu().pin_memory()
         b_h = b[0].cpu().pin_memory()
         c_h = torch.empty((3, n), dtype=torch.int32).pin_memory()
-        mc.mul_three_primes_tensor(a_h, b_h, out=c).cpu()
-        torch.cuda.synchronize()
-        barrier()
-        ev3 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-               for _ in range(args.steps)]
-        for i in range(args.steps):
-            flush.zero_()
-            ev3[i][0].record(stream)
-            cc = mc.mul_three_primes_tensor(a_h, b_h, out=c)
-            c_h.copy_(cc, non_blocking=True)
-            ev3[i][1].record(stream)
-        barrier()
-        t3 = sum(s.elapsed_time(e) for s, e in ev3)
-        e2e = {"value": args.steps / (t3 / 1e3), "unit": "products/s",
-               "h2d_bytes_per_step": 4 * (z1 + z2), "d2h_bytes_per_step": 12 * n}
+        if ws > 1:
+            from paper_1609_01010_b200.distributed import mul_three_primes_p2p
 
+            def e2e_step():
+                x = a_h.to(dev, non_blocking=True)
+                y = b_h.to(dev, non_blocking=True)
+                r = mul_three_primes_p2p(x, y, dst=0)
+                if r is not None:
+                    c_h.copy_(r, non_blocking=True)
+        else:
+            def e2e_step():
+                c_h.copy_(mc.mul_three_primes_tensor(a_h, b_h, out=c), non_blocking=True)
+        h2d, d2h = 4 * (z1 + z2) * ws, 12 * n
+    for _ in range(max(1, args.warmup)):
+        e2e_step()
+    torch.cuda.synchronize()
+    ev2 = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    barrier()
+    for i in range(args.steps):
+        flush.zero_()
+        ev2[i][0].record(stream)
+        e2e_step()
+        ev2[i][1].record(stream)
+    barrier()
+    t2 = _allreduce([sum(s.elapsed_time(e) for s, e in ev2)], "max", dev)[0]
+    if rows and (engine != "three_primes" or rank == 0):
+        assert torch.equal(c_h.to(dev), c), "e2e output differs from the device-resident output"
+    e2e = {"value": products * args.steps / (t2 / 1e3), "unit": "products/s",
+           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+           "path": "conv_batch on page-locked host tensors (mc_conv_host_async)"
+           if engine != "three_primes" else
+           "pinned host inputs -> mul_three_primes -> pinned host limbs"}
+    del a, b, c, flush, a_h, b_h, c_h
+    graph = None
+    torch.cuda.empty_cache()
+
+    alg, note = bytes_model(cfg)
+    kern_ms = t_max / args.steps  # max-over-ranks device time per step
+    peak, peak_kind, peaks = _peaks()
+    # per GPU: the bytes this rank's share moved / its step time (ranks equal
+    # to within one product)
+    alg_gpu = alg if mode == "replicas" else alg / ws
+    achieved = alg_gpu / (kern_ms / 1e3) / 1e9
+    bf, pw = butterflies(cfg)
+    rec = {
+        "config": config_dict(cfg),
+        "partition": {"mode": mode, "ranks": ws, "rows_this_rank": rows,
+                      "rows_all_ranks": int(rows_all)},
+        "ms_per_step": kern_ms, "value": value, "unit": "products/s",
+        "gcoeff_per_s": value * n / 1e9,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_kind": peak_kind,
+                     "alg_bytes_per_step": alg, "bytes_model": note, "kernel_ms": kern_ms,
+                     "per": "GPU"},
+        "int_pipe": _int_roofline(bf, pw, value / ws, peaks, lazy_share(cfg)),
+        "e2e": e2e,
+        "gpu_launches": int(launches_all),
+        "launch": "cuda graph replay" if launches_per_step is not None else "eager",
+        "clocks": clk,
+    }
+    try:  # DRAM bytes and pipe utilisation per launch from a committed ncu capture
+        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
+            tr = json.load(f).get(cfg["name"])
+        if tr:
+            rec["roofline"]["traffic"] = tr["dram_bytes_read"] + tr["dram_bytes_write"]
+            rec["roofline"]["traffic_source"] = tr.get("source")
+            if tr.get("ncu_pipes"):
+                rec["int_pipe"]["ncu"] = tr["ncu_pipes"]
+    except Exception:
+        pass
+    rec["roofline"].setdefault("traffic", None)
+    return rec
+
+
+def run_mine(args, cfg_ids) -> None:
+    import torch
+
+    ws, rank, local = _dist()
+    init_dist(ws, local, gpu=True)
+    if ws <= 1:
+        torch.cuda.set_device(0)
+    prev_affinity = _bind_local_cpus(torch.cuda.current_device())
+    recs = {c: measure(CONFIGS[c], args, ws, rank) for c in cfg_ids}
     if rank != 0:
         if ws > 1:
             torch.distributed.destroy_process_group()
         return
-
-    peak, peak_kind, peaks = _peaks()
-    if engine == "three_primes":
-        # compulsory I/O plus the four-step pass model per prime
-        alg_bytes = 4 * (z1 + z2) + 12 * n + 3 * 4 * 6 * L
-        bytes_note = "4*(z1+z2) in + 12*n limbs out + 3 primes x 4*6L four-step passes"
-    elif L > 8192:
-        alg_bytes = 4 * (z1 + z2 + n + 6 * L) * B
-        bytes_note = "four-step pass model 4*(z1+z2+n+6L) per product"
-    else:
-        alg_bytes = 4 * (z1 + z2 + n) * B
-        bytes_note = "compulsory 4*(z1+z2+n) per product (fused single pass)"
-    kern_ms = statistics.mean(times)  # one launch of the fused kernel per step (cfg 1-3)
-    traffic, ncu_pipes = None, None
-    try:  # DRAM bytes and pipe utilisation per launch from the committed ncu capture
-        with open(os.path.join(REPO, "profiles", "traffic.json")) as f:
-            tr = json.load(f).get(cfg["name"])
-        if tr:
-            traffic = tr["dram_bytes_read"] + tr["dram_bytes_write"]
-            ncu_pipes = tr.get("ncu_pipes")
-    except Exception:
-        traffic = None
-    achieved = alg_bytes / (kern_ms / 1e3) / 1e9
-    from paper_1609_01010_b200.transform import full_count, itft_count, tft_count
-
-    if engine == "tft":
-        bf = tft_count(L, z1, n) + tft_count(L, z2, n) + itft_count(L, n)
-        pw = n
-    elif engine == "fft_pad":
-        bf, pw = 3 * full_count(L), L
-    else:
-        bf, pw = 3 * 3 * full_count(L), 3 * L
-    if prev_affinity:  # the CPU baseline uses every host thread again
+    if prev_affinity:  # the CPU baselines use every host thread again
         os.sched_setaffinity(0, prev_affinity)
-    cpu_rate, sample, cpu_cores = cpu_oracle_rate(cfg, host_threads(), target_s=args.ref_seconds)
+    for c in cfg_ids:
+        tgt = args.ref_seconds if c == args.config else args.ref_seconds_other
+        rate, sample, cores = cpu_oracle_rate(CONFIGS[c], host_threads(), target_s=tgt)
+        recs[c]["cpu_baseline"] = {"value": rate, "unit": "products/s", "cores": cores,
+                                   "kind": "port", "sample": sample}
+    head = recs[args.config]
+    strong = head["partition"]["mode"] != "replicas"
     line = {
-        "metric": "modular poly-mults/sec", "value": value, "unit": "products/s",
-        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "metric": METRIC, "value": head["value"], "unit": "products/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
         "higher_is_better": True, "scaling": "strong" if strong else "weak",
         "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded splitmix64 uniform residues, generated on device)",
-        "config": {"workload": cfg["name"], "batch_per_rank": B, "global_batch": B * ws,
-                   "z1": z1, "z2": z2, "n": n, "L": L, "p": p, "engine": engine,
-                   "parallelism": f"dp{ws} (independent products)",
-                   "l2": "flushed (256 MiB write) before every timed step",
-                   "launch": "cuda graph replay" if graph is not None else "eager"},
-        "gcoeff_per_s": value * n / 1e9,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_kind": peak_kind,
-                     "alg_bytes_per_step": alg_bytes, "bytes_model": bytes_note,
-                     "kernel_ms": kern_ms},
-        "int_pipe": dict(_int_roofline(bf, pw, value / ws, peaks, lazy_share(cfg)),
-                         **({"ncu": ncu_pipes} if ncu_pipes else {})),
-        "e2e": e2e,
-        "gpu_launches": launches,
-        "clocks": clk,
-        "cpu_baseline": {"value": cpu_rate, "unit": "products/s", "cores": cpu_cores,
-                         "kind": "port", "sample": sample},
+        "config": head["config"],
+        "run": {"partition": head["partition"],
+                "parallelism": f"{ws} rank(s), one GPU each; "
+                               + {"shards": "global batch partitioned (no collective)",
+                                  "replicas": "replicas",
+                                  "primes": "primes over ranks, CRT gather over peer memory"}[
+                                   head["partition"]["mode"]],
+                "l2": "flushed (256 MiB write) before every timed step",
+                "launch": head["launch"], "timing": "CUDA events, max over ranks"},
+        "gcoeff_per_s": head["gcoeff_per_s"],
+        "roofline": head["roofline"], "int_pipe": head["int_pipe"], "e2e": head["e2e"],
+        "gpu_launches": head["gpu_launches"], "clocks": head["clocks"],
+        "cpu_baseline": head["cpu_baseline"],
+        "all_configs": {f"cfg{c}": recs[c] for c in cfg_ids},
     }
     print(json.dumps(line), flush=True)
     if ws > 1:
         torch.distributed.destroy_process_group()
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args, cfg_ids) -> None:
+    """--impl reference: the reference path's CPU implementation (the C
+    oracle port; the reference itself is pure Python and does not travel to
+    the GPU box) with all host threads, on the same configs, metric and
+    config dicts as the GPU arm.  Under torchrun only rank 0 runs."""
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    from oracle import oracle
+
+    oracle.lib()
+    threads = host_threads()
+    cfg = CONFIGS[args.config]
+    rates, sample, used = [], None, threads
+    for i in range(args.warmup + args.steps):
+        r, sample, used = cpu_oracle_rate(cfg, threads, target_s=args.ref_step_seconds)
+        if i >= args.warmup:
+            rates.append(r)
+    v = statistics.median(rates)
+    others = {}
+    for c in cfg_ids:
+        if c == args.config:
+            continue
+        r, s, u = cpu_oracle_rate(CONFIGS[c], threads, target_s=args.ref_seconds_other)
+        others[f"cfg{c}"] = {"config": config_dict(CONFIGS[c]), "value": r, "unit": "products/s",
+                             "cpu_baseline": {"value": r, "unit": "products/s", "cores": u,
+                                              "kind": "port", "sample": s}}
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "products/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * cfg["batch"] / v, "higher_is_better": True,
+        "scaling": "strong" if cfg["batch"] > 1 or cfg["engine"] == "three_primes" else "weak",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic (seeded splitmix64)",
+        "config": config_dict(cfg),
+        "gcoeff_per_s": v * (cfg["z1"] + cfg["z2"] - 1) / 1e9,
+        "cpu_baseline": {"value": v, "unit": "products/s", "cores": used, "kind": "port",
+                         "sample": sample + " per step; C restatement of the reference "
+                                            "(oracle/modconv_oracle.c)"},
+        "e2e": {"value": v, "unit": "products/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "all_configs": dict({f"cfg{args.config}": {"config": config_dict(cfg), "value": v,
+                                                    "unit": "products/s"}}, **others),
+    }
+    print(json.dumps(line), flush=True)
 
 
 def main():
@@ -528,25 +700,40 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
+    ap.add_argument("--config", type=int, default=HEADLINE, choices=sorted(CONFIGS),
+                    help="the config of the top-level line")
+    ap.add_argument("--configs", default="1,2,3,4,5",
+                    help="configs measured in the run (all_configs); 'head' = --config only")
     ap.add_argument("--impl", default="mine", choices=["mine", "reference"])
     ap.add_argument("--engine", default=None, choices=["tft", "fft_pad"],
-                    help="override the config's engine (analysis only)")
+                    help="override the headline config's engine (analysis only)")
+    ap.add_argument("--plan-only", action="store_true",
+                    help="multi-rank partition plumbing only, no kernels (CPU)")
     ap.add_argument("--ref-seconds", type=float, default=10.0,
-                    help="target CPU seconds of the cpu_baseline sample")
+                    help="target CPU seconds of the headline cpu_baseline sample")
+    ap.add_argument("--ref-seconds-other", type=float, default=4.0,
+                    help="target CPU seconds of the other configs' cpu_baseline samples")
     ap.add_argument("--ref-step-seconds", type=float, default=2.0,
                     help="target CPU seconds per --impl reference step")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
-    cfg = dict(CONFIGS[args.config])
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch(args))
+    ids = [args.config] if args.configs == "head" else \
+        [int(x) for x in args.configs.split(",") if x.strip()]
+    if args.config not in ids:
+        ids.insert(0, args.config)
+    ids = [args.config] + [c for c in ids if c != args.config]  # headline first
     if args.engine:  # analysis override (e.g. fft_pad on config 2's shapes)
-        cfg["engine"] = args.engine
-        cfg["name"] += f"_engine_{args.engine}"
-    if args.impl == "reference":
-        run_reference(args, cfg)
+        CONFIGS[args.config] = dict(CONFIGS[args.config], engine=args.engine,
+                                    name=CONFIGS[args.config]["name"] + f"_engine_{args.engine}")
+    if args.plan_only:
+        plan_only(args, ids)
+    elif args.impl == "reference":
+        run_reference(args, ids)
     else:
-        run_mine(args, cfg)
+        run_mine(args, ids)
 
 
 if __name__ == "__main__":

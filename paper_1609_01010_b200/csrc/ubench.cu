@@ -10,6 +10,18 @@
 
 namespace mc {
 
+// Shoup-style lazy product with the quotient estimated on the FP64 pipe
+// instead of IMAD.HI: q = floor(x * wd) with wd = RD(w / p) (one DADD makes x
+// exact in a double, one DFMA.RZ adds 2^52 so the integer quotient lands in
+// the low mantissa word), r = x*w - q*p in [0, 2p) as with Shoup.  Probe of
+// whether the FP64 pipe can take the high-product half of the work.
+__device__ __forceinline__ u32 mul_f64q_lazy(u32 x, u32 w, double wd, u32 p) {
+    const double xd = __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
+    const double qd = __fma_rz(xd, wd, 4503599627370496.0);
+    const u32 q = (u32)__double2loint(qd);
+    return x * w - q * p;
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(256) ubench_kernel(u32 *out, u32 seed, int iters, u32 p,
                                                      u32 wp) {
@@ -30,6 +42,14 @@ __global__ void __launch_bounds__(256) ubench_kernel(u32 *out, u32 seed, int ite
                     u32 a = x[i], b = x[(i + 1) & 7];
                     bfly_dit(a, b, p - 7, wp, p);
                     x[i] = a ^ b;
+                }
+                if (KIND == 6) {                                           // DFMA chain
+                    double d = __hiloint2double((int)wp, (int)x[i]);
+                    d = fma(d, 1.0000001, 0.5);
+                    x[i] = (u32)__double2loint(d);
+                }
+                if (KIND == 7) {                                           // f64-quotient mul
+                    x[i] = red1(mul_f64q_lazy(x[i], p - 7, (double)(p - 7) / p, p), p);
                 }
             }
         }
@@ -58,10 +78,16 @@ __device__ __forceinline__ void bfly_variant(u32 &a, u32 &b, u32 w, u32 wp, u32 
         const u32 s = __viaddmin_u32(a, b, a + b - 2 * p);
         b = mul_shoup_lazy(a - b + 2 * p, w, wp, p);
         a = s;
-    } else {
+    } else if (MODE == 3) {
         const u32 s = a + b;
         b = mul_shoup_lazy(a - b + 2 * p, w, wp, p);
         a = min(s, s - 2 * p);
+    } else {  // MODE 4: canonical, quotient on the FP64 pipe (wp holds an index)
+        const u32 s = a + b;
+        const u32 r = mul_f64q_lazy(a - b + p, w, __longlong_as_double(
+            ((long long)wp << 32) | w), p);
+        a = min(s, s - p);
+        b = min(r, r - p);
     }
 }
 
@@ -106,7 +132,7 @@ extern "C" {
 
 // Butterflies per clock per SM of the isolated register pass:
 // rates[0] MODE 0 at 2 CTAs/SM, rates[1] MODE 0 at 4 CTAs/SM,
-// rates[2..4] MODES 1..3 at 2 CTAs/SM (see bfly_variant).
+// rates[2..5] MODES 1..4 at 2 CTAs/SM (see bfly_variant).
 mc_status mc_ubench_pass(double *rates) {
     using namespace mc;
     const int sms = sm_count();
@@ -129,7 +155,7 @@ mc_status mc_ubench_pass(double *rates) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int iters = 200;
-    for (int k = 0; k < 5; ++k) {
+    for (int k = 0; k < 6; ++k) {
         const int per_sm = k == 1 ? 4 : 2;
         const int blocks = sms * per_sm;
         for (int rep = 0; rep < 2; ++rep) {
@@ -140,6 +166,7 @@ mc_status mc_ubench_pass(double *rates) {
                 case 2: pass_bench_kernel<2, 1><<<blocks, 256>>>(tw, out, iters, p); break;
                 case 3: pass_bench_kernel<2, 2><<<blocks, 256>>>(tw, out, iters, p); break;
                 case 4: pass_bench_kernel<2, 3><<<blocks, 256>>>(tw, out, iters, p); break;
+                case 5: pass_bench_kernel<2, 4><<<blocks, 256>>>(tw, out, iters, p); break;
             }
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
@@ -172,7 +199,7 @@ mc_status mc_ubench_int_pipes(double *rates, int nkinds, double *sm_mhz) {
     const int iters = 512, blocks = sms * 8, threads = 256;
     const u32 p = 2013265921u;
     const u32 wp = (u32)(((u64)(p - 7) << 32) / p);
-    for (int k = 0; k < nkinds && k < 6; ++k) {
+    for (int k = 0; k < nkinds && k < 8; ++k) {
         for (int rep = 0; rep < 2; ++rep) {
             cudaEventRecord(e0);
             switch (k) {
@@ -182,6 +209,8 @@ mc_status mc_ubench_int_pipes(double *rates, int nkinds, double *sm_mhz) {
                 case 3: ubench_kernel<3><<<blocks, threads>>>(out, 7, iters, p, wp); break;
                 case 4: ubench_kernel<4><<<blocks, threads>>>(out, 7, iters, p, wp); break;
                 case 5: ubench_kernel<5><<<blocks, threads>>>(out, 7, iters, p, wp); break;
+                case 6: ubench_kernel<6><<<blocks, threads>>>(out, 7, iters, p, wp); break;
+                case 7: ubench_kernel<7><<<blocks, threads>>>(out, 7, iters, p, wp); break;
             }
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);

@@ -177,6 +177,30 @@ def close_peer_buffers(group=None) -> None:
     _PEER_CACHE.clear()
 
 
+def _stream_barrier(group, device) -> None:
+    """Barrier ordered on the current CUDA stream.
+
+    Under NCCL: a one-word all-reduce.  Its kernel on every rank starts only
+    after the work already queued on that rank's stream and ends only when
+    every rank has contributed, and the caller's stream waits on it on the
+    device -- so after it, every rank's earlier kernels are done, with no
+    host synchronization and no host round trip.  Under a host backend
+    (gloo: CPU tests, one shared GPU) the host synchronizes its stream and
+    meets the others in dist.barrier."""
+    if dist.get_backend(group) == "nccl":
+        flag = _BARRIER_WORDS.get(device)
+        if flag is None:
+            flag = _BARRIER_WORDS[device] = torch.zeros(1, dtype=torch.int32, device=device)
+        dist.all_reduce(flag, group=group)
+    else:
+        if device.type == "cuda":
+            torch.cuda.current_stream(device).synchronize()
+        dist.barrier(group=group)
+
+
+_BARRIER_WORDS: dict = {}
+
+
 def mul_three_primes_p2p(a: torch.Tensor, b: torch.Tensor, dst: int = 0, group=None):
     """Exact integer product of a and b (int32 words on this rank's GPU,
     identical on every rank), primes spread over the ranks; the residue
@@ -187,7 +211,10 @@ def mul_three_primes_p2p(a: torch.Tensor, b: torch.Tensor, dst: int = 0, group=N
     its coefficient slice (shard_rows(n, ws, r)), loading the three residue
     planes from their owners' GPUs and storing its limbs straight into
     dst's buffer over NVLink; after a second barrier dst copies the limbs
-    out.  Returns [3, n] int32 limbs on dst, None elsewhere.
+    out.  Under NCCL both barriers are stream-ordered one-word all-reduces
+    (_stream_barrier): the call enqueues everything and returns without a
+    host synchronization.  Returns [3, n] int32 limbs on dst, None
+    elsewhere.
     """
     from . import _native, _tensors
 
@@ -209,13 +236,13 @@ def mul_three_primes_p2p(a: torch.Tensor, b: torch.Tensor, dst: int = 0, group=N
     for k in primes_of_rank(ws, rank):
         _native.check(lib.mc_mul_mod_prime_k(a_.data_ptr(), z1, b_.data_ptr(), z2,
                                              st.res[rank] + 4 * k * n, k, stream))
-    torch.cuda.current_stream().synchronize()
-    dist.barrier(group=group)  # every residue plane is written
+    _stream_barrier(group, a.device)  # every residue plane is written
     lo, cnt = shard_rows(n, ws, rank)
     r = [st.res[k % ws] + 4 * (k * n + lo) for k in range(3)]
     _native.check(lib.mc_crt3_slice(r[0], r[1], r[2], st.out + 4 * lo, n, cnt, stream))
-    torch.cuda.current_stream().synchronize()
-    dist.barrier(group=group)  # every limb slice is in dst's buffer
+    # every limb slice is in dst's buffer, and no rank reads a residue plane
+    # any more (the next call may overwrite them)
+    _stream_barrier(group, a.device)
     if rank != dst:
         return None
     out = torch.empty((3, n), dtype=torch.int32, device=a.device)

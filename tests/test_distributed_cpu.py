@@ -92,3 +92,55 @@ def test_three_primes_gather_gloo(tmp_path, orc, ws):
     assert np.array_equal(limbs, orc.mul_three_primes(a, b))
     calls = sorted(int(k) for r in range(ws) for k in np.load(tmp_path / f"calls_{r}.npy"))
     assert calls == [0, 1, 2]  # every prime computed exactly once
+
+
+@pytest.mark.parametrize("ws", [2, 3])
+def test_bench_self_launches_ranks(ws):
+    """`bench.py --gpus N` outside torchrun re-launches itself with N ranks;
+    every config's global batch is partitioned over them (strong scaling):
+    the shards tile the batch exactly, config 1 runs as replicas and
+    config 5 spreads its primes."""
+    import json
+    import subprocess
+
+    env = dict(os.environ, BENCH_BACKEND="gloo")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(REPO, "bench.py"), "--gpus", str(ws),
+                        "--plan-only"], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == ws
+    cfgs = line["configs"]
+    assert list(cfgs)[0] == "cfg2"  # the headline config first
+    for name, batch in (("cfg2", 4096), ("cfg3", 65536), ("cfg4", 8)):
+        c = cfgs[name]
+        assert c["mode"] == "shards"
+        assert c["config"]["global_batch"] == batch == c["covered_rows"]
+        spans = c["ranges"]
+        assert len(spans) == ws and spans[0][0] == 0
+        assert all(a[0] + a[1] == b[0] for a, b in zip(spans, spans[1:]))
+    assert cfgs["cfg1"]["mode"] == "replicas" and cfgs["cfg1"]["global_products"] == ws
+    assert cfgs["cfg5"]["mode"] == "primes" and cfgs["cfg5"]["global_products"] == 1
+
+
+def _barrier_worker(rank, ws, port, out_dir):
+    sys.path.insert(0, REPO)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    from paper_1609_01010_b200.distributed import _stream_barrier
+
+    import time
+
+    time.sleep(0.2 * rank)
+    _stream_barrier(None, torch.device("cpu"))
+    with open(os.path.join(out_dir, f"t{rank}"), "w") as f:
+        f.write(repr(time.time()))
+    dist.destroy_process_group()
+
+
+def test_stream_barrier_host_backend(tmp_path):
+    """Under a host backend the p2p CRT's barrier meets every rank."""
+    mp.spawn(_barrier_worker, args=(3, _free_port(), str(tmp_path)), nprocs=3, join=True)
+    ts = [float(open(tmp_path / f"t{r}").read()) for r in range(3)]
+    assert max(ts) - min(ts) < 0.3

@@ -87,7 +87,8 @@ def test_poly_mul_returns_callers_class(engine):
     z = mc.poly_mul(ForeignPoly(ff, (0, 0)), ForeignPoly(ff, v), mc.ConvRequest(ff, engine=engine))
     assert z == ForeignPoly(ff, ())
     # this package's own class keeps the operands' field object
-    own = mc.poly_mul(mc.DensePoly(ref, u), mc.DensePoly(ref, v), mc.ConvRequest(ref))
+    own = mc.poly_mul(mc.DensePoly(ref, u), mc.DensePoly(ref, v),
+                      mc.ConvRequest(ref, engine=engine))
     assert own.field is ref
 
 
