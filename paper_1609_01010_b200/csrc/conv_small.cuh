@@ -100,7 +100,35 @@ __device__ __forceinline__ uint2 ldtw(const uint2 *tab, int i) { return tab[i]; 
 struct Tw {
     const uint2 *tf;  // shared-memory copy of P.tf
     const uint2 *ti;  // shared-memory copy of P.ti
+    static constexpr bool kNeg = false;
 };
+
+// Merged stage table (half the shared memory of tf + ti): stage h = 2^lg
+// holds w_{2h}^k for k = 0..h at m[h + lg - 1 + k].  Forward twiddle
+// w_{2h}^j = m[h + lg - 1 + j]; inverse twiddle w_{2h}^-j = -w_{2h}^(h-j) =
+// -m[2h + lg - 1 - j] (j = 0 reads w_{2h}^h = -1), so the inverse butterflies
+// take the mirrored entry and swap their outputs (bfly_dit_neg_t).  Lanes read
+// consecutive (or reverse-consecutive) entries, so the accesses stay
+// conflict-free.
+struct TwM {
+    const uint2 *m;
+    static constexpr bool kNeg = true;
+};
+
+__device__ __forceinline__ uint2 tw_fwd(const Tw &W, int h, int, int j) { return W.tf[h + j]; }
+__device__ __forceinline__ uint2 tw_fwd(const TwM &W, int h, int lg, int j) {
+    return W.m[h + lg - 1 + j];
+}
+__device__ __forceinline__ uint2 tw_inv(const Tw &W, int h, int, int j) { return W.ti[h + j]; }
+__device__ __forceinline__ uint2 tw_inv(const TwM &W, int h, int lg, int j) {
+    return W.m[2 * h + lg - 1 - j];
+}
+
+template <int AR, class TW>
+__device__ __forceinline__ void bfly_dit_tw(u32 &a, u32 &b, uint2 w, u32 p) {
+    if constexpr (TW::kNeg) bfly_dit_neg_t<AR>(a, b, w.x, w.y, p);
+    else bfly_dit_t<AR>(a, b, w.x, w.y, p);
+}
 
 // ---------------------------------------------------------------- top pass (forward)
 // Stages with half-size h = H*G, H = 8, 4, 2, 1 on slots (s, s+H).  All
@@ -117,9 +145,9 @@ struct Tw {
 // step is a bare Montgomery product.  The kernel always scales operand a,
 // which the host makes the shorter one: at most 8 slots per thread against
 // the >= 9 active slots of the pointwise step.
-template <int K, int NT, int ZS, int AR = 0, bool SCALE = false>
+template <int K, int NT, int ZS, int AR = 0, bool SCALE = false, class TW = Tw>
 __device__ __forceinline__ void fwd_top_zs(u32 (&v)[16], int t, const ConvSmallParams &P,
-                                           const Tw &W) {
+                                           const TW &W) {
     constexpr int G = 1 << (K - 4);
     const u32 p = P.p;
     if constexpr (SCALE) {
@@ -141,13 +169,13 @@ __device__ __forceinline__ void fwd_top_zs(u32 (&v)[16], int t, const ConvSmallP
             const bool hi_zero = so + H >= ZS;
             if (!hi_zero) {
                 if (hi_needed) {
-                    const uint2 w = ldtw(W.tf, h + t + G * so);
+                    const uint2 w = tw_fwd(W, h, lv + K - 4, t + G * so);
                     bfly_dif_t<AR>(v[s], v[s + H], w.x, w.y, p);
                 } else {
                     v[s] = add_t<AR>(v[s], v[s + H], p);  // lo-only add (fold)
                 }
             } else if (hi_needed) {
-                const uint2 w = ldtw(W.tf, h + t + G * so);
+                const uint2 w = tw_fwd(W, h, lv + K - 4, t + G * so);
                 v[s + H] = mul_t<AR>(v[s], w.x, w.y, p);  // hi input is zero
             }
         }
@@ -160,28 +188,28 @@ __device__ __forceinline__ void fwd_top_zs(u32 (&v)[16], int t, const ConvSmallP
 #define MC_ZS_STEP 4
 #endif
 
-template <int K, int NT, int AR = 0, bool SCALE = false>
+template <int K, int NT, int AR = 0, bool SCALE = false, class TW = Tw>
 __device__ __forceinline__ void fwd_top(u32 (&v)[16], int z, int t, const ConvSmallParams &P,
-                                        const Tw &W) {
+                                        const TW &W) {
     constexpr int G = 1 << (K - 4);
     const int zs = (z + G - 1) / G;  // uniform across the launch
 #if MC_ZS_STEP == 2
-    if (zs <= 2) fwd_top_zs<K, NT, 2, AR, SCALE>(v, t, P, W);
-    else if (zs <= 4) fwd_top_zs<K, NT, 4, AR, SCALE>(v, t, P, W);
-    else if (zs <= 6) fwd_top_zs<K, NT, 6, AR, SCALE>(v, t, P, W);
-    else if (zs <= 8) fwd_top_zs<K, NT, 8, AR, SCALE>(v, t, P, W);
-    else if (zs <= 10) fwd_top_zs<K, NT, 10, AR, SCALE>(v, t, P, W);
-    else if (zs <= 12) fwd_top_zs<K, NT, 12, AR, SCALE>(v, t, P, W);
-    else if (zs <= 14) fwd_top_zs<K, NT, 14, AR, SCALE>(v, t, P, W);
-    else fwd_top_zs<K, NT, 16, AR, SCALE>(v, t, P, W);
+    if (zs <= 2) fwd_top_zs<K, NT, 2, AR, SCALE, TW>(v, t, P, W);
+    else if (zs <= 4) fwd_top_zs<K, NT, 4, AR, SCALE, TW>(v, t, P, W);
+    else if (zs <= 6) fwd_top_zs<K, NT, 6, AR, SCALE, TW>(v, t, P, W);
+    else if (zs <= 8) fwd_top_zs<K, NT, 8, AR, SCALE, TW>(v, t, P, W);
+    else if (zs <= 10) fwd_top_zs<K, NT, 10, AR, SCALE, TW>(v, t, P, W);
+    else if (zs <= 12) fwd_top_zs<K, NT, 12, AR, SCALE, TW>(v, t, P, W);
+    else if (zs <= 14) fwd_top_zs<K, NT, 14, AR, SCALE, TW>(v, t, P, W);
+    else fwd_top_zs<K, NT, 16, AR, SCALE, TW>(v, t, P, W);
 #elif MC_ZS_STEP == 4
-    if (zs <= 4) fwd_top_zs<K, NT, 4, AR, SCALE>(v, t, P, W);
-    else if (zs <= 8) fwd_top_zs<K, NT, 8, AR, SCALE>(v, t, P, W);
-    else if (zs <= 12) fwd_top_zs<K, NT, 12, AR, SCALE>(v, t, P, W);
-    else fwd_top_zs<K, NT, 16, AR, SCALE>(v, t, P, W);
+    if (zs <= 4) fwd_top_zs<K, NT, 4, AR, SCALE, TW>(v, t, P, W);
+    else if (zs <= 8) fwd_top_zs<K, NT, 8, AR, SCALE, TW>(v, t, P, W);
+    else if (zs <= 12) fwd_top_zs<K, NT, 12, AR, SCALE, TW>(v, t, P, W);
+    else fwd_top_zs<K, NT, 16, AR, SCALE, TW>(v, t, P, W);
 #else
-    if (zs <= 8) fwd_top_zs<K, NT, 8, AR, SCALE>(v, t, P, W);
-    else fwd_top_zs<K, NT, 16, AR, SCALE>(v, t, P, W);
+    if (zs <= 8) fwd_top_zs<K, NT, 8, AR, SCALE, TW>(v, t, P, W);
+    else fwd_top_zs<K, NT, 16, AR, SCALE, TW>(v, t, P, W);
 #endif
 }
 
@@ -192,9 +220,9 @@ __device__ __forceinline__ void fwd_top(u32 (&v)[16], int z, int t, const ConvSm
 #endif
 
 // ---------------------------------------------------------------- lower passes
-template <int K, int LO, int HI, int SB, int AR = 0>
+template <int K, int LO, int HI, int SB, int AR = 0, class TW = Tw>
 __device__ __forceinline__ void fwd_lower(u32 (&v)[16], int t, const ConvSmallParams &P,
-                                          const Tw &W) {
+                                          const TW &W) {
     const u32 p = P.p;
     const int tpos = slot_pos<SB>(t, 0);
 #pragma unroll
@@ -215,15 +243,15 @@ __device__ __forceinline__ void fwd_lower(u32 (&v)[16], int t, const ConvSmallPa
                 continue;
             }
             const int j = (tpos | (s << SB)) & (h - 1);
-            const uint2 w = ldtw(W.tf, h + j);
+            const uint2 w = tw_fwd(W, h, b, j);
             bfly_dif_t<AR>(v[s], v[s | (1 << sbit)], w.x, w.y, p);
         }
     }
 }
 
-template <int K, int LO, int HI, int SB, int AR = 0>
+template <int K, int LO, int HI, int SB, int AR = 0, class TW = Tw>
 __device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallParams &P,
-                                          const Tw &W) {
+                                          const TW &W) {
     const u32 p = P.p;
     const int tpos = slot_pos<SB>(t, 0);
 #pragma unroll
@@ -244,8 +272,8 @@ __device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallPa
                 continue;
             }
             const int j = (tpos | (s << SB)) & (h - 1);
-            const uint2 w = ldtw(W.ti, h + j);
-            bfly_dit_t<AR>(v[s], v[s | (1 << sbit)], w.x, w.y, p);
+            const uint2 w = tw_inv(W, h, b, j);
+            bfly_dit_tw<AR, TW>(v[s], v[s | (1 << sbit)], w, p);
         }
     }
 }
@@ -259,8 +287,9 @@ __device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallPa
 // (Shoup products accept any word).  Outputs are in the mode's inverse range.
 template <int K, int M, int N, int OFF, int AR = 0>
 struct ItftTop {
+    template <class TW>
     static __device__ __forceinline__ void run(u32 (&v)[16], int t, const ConvSmallParams &P,
-                                               const Tw &W) {
+                                               const TW &W) {
         constexpr int G = 1 << (K - 4);
         constexpr int H = M / 2;
         constexpr int LV = (M == 16) ? 4 : (M == 8) ? 3 : (M == 4) ? 2 : 1;
@@ -288,7 +317,7 @@ struct ItftTop {
 #pragma unroll
             for (int s = N - H; s < H; ++s) {  // cross butterflies
                 const u32 a = canon_t<AR>(v[OFF + s], p), b = canon_t<AR>(v[OFF + s + H], p);
-                const uint2 w = ldtw(W.tf, h + t + G * s);
+                const uint2 w = tw_fwd(W, h, LV - 1 + K - 4, t + G * s);
                 u32 d = sub_mod(mul_shoup(a, ih, p), add_mod(b, b, p), p);
                 v[OFF + s + H] = mul_shoup(d, w.x, w.y, p);
                 v[OFF + s] = sub_mod(add_mod(a, a, p), mul_shoup(b, mm, p), p);
@@ -296,8 +325,8 @@ struct ItftTop {
             ItftTop<K, H, N - H, OFF + H, AR>::run(v, t, P, W);
 #pragma unroll
             for (int s = 0; s < N - H; ++s) {  // inverse DIT butterflies
-                const uint2 w = ldtw(W.ti, h + t + G * s);
-                bfly_dit_t<AR>(v[OFF + s], v[OFF + s + H], w.x, w.y, p);
+                const uint2 w = tw_inv(W, h, LV - 1 + K - 4, t + G * s);
+                bfly_dit_tw<AR, TW>(v[OFF + s], v[OFF + s + H], w, p);
             }
         }
     }
@@ -305,9 +334,9 @@ struct ItftTop {
 
 // Inverse top pass (complete or truncated) in mode AR; outputs in the mode's
 // inverse range (canon_t before storing).
-template <int K, int NT, int AR>
+template <int K, int NT, int AR, class TW = Tw>
 __device__ __forceinline__ void inv_top(u32 (&v)[16], int t, const ConvSmallParams &P,
-                                        const Tw &W) {
+                                        const TW &W) {
     ItftTop<K, 16, NT, 0, AR>::run(v, t, P, W);
 }
 
@@ -404,9 +433,9 @@ __device__ __forceinline__ bool pass_active(int t) {
     else return gblock_of_pass<K, I>(t & ~31) < NT;  // warp-uniform
 }
 
-template <int K, int NT, int I, int AR = 0>
+template <int K, int NT, int I, int AR = 0, class TW = Tw>
 __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[16], u32 (&vb)[16],
-                                                int t, const ConvSmallParams &P, const Tw &W) {
+                                                int t, const ConvSmallParams &P, const TW &W) {
     if constexpr (I < Plan<K>::NP) {
         constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         constexpr int SB = Plan<K>::sb(I);
@@ -419,36 +448,36 @@ __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[
         // Inactive G-blocks (>= NT) are skipped per warp where possible;
         // otherwise transformed and discarded at the pointwise step.
         if (pass_active<K, I, NT>(t)) {
-            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR>(va, t, P, W);
-            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR>(vb, t, P, W);
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(va, t, P, W);
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(vb, t, P, W);
         }
-        fwd_lower_chain<K, NT, I + 1, AR>(bufA, bufB, va, vb, t, P, W);
+        fwd_lower_chain<K, NT, I + 1, AR, TW>(bufA, bufB, va, vb, t, P, W);
     }
 }
 
 // Inverse lower passes in reverse order (lowest bits first); on exit the
 // slots are in the top-pass layout.
-template <int K, int NT, int I, int AR = 0>
+template <int K, int NT, int I, int AR = 0, class TW = Tw>
 __device__ __forceinline__ void inv_lower_chain(u32 *buf, u32 (&v)[16], int t,
-                                                const ConvSmallParams &P, const Tw &W) {
+                                                const ConvSmallParams &P, const TW &W) {
     if constexpr (I >= 0) {
         constexpr int SB = Plan<K>::sb(I);
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         if (pass_active<K, I, NT>(t))
-            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR>(v, t, P, W);  // zeros stay zeros
+            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v, t, P, W);  // zeros stay zeros
         __syncthreads();
         put<SB>(buf, v, t);
         __syncthreads();
         get<SBnext>(buf, v, t);
-        inv_lower_chain<K, NT, I - 1, AR>(buf, v, t, P, W);
+        inv_lower_chain<K, NT, I - 1, AR, TW>(buf, v, t, P, W);
     }
 }
 
 // One operand, arbitrary layout: forward lower passes; on exit the slots
 // are in the last lower pass's layout.
-template <int K, int I, class Lay, int NT = 16, int AR = 0>
+template <int K, int I, class Lay, int NT = 16, int AR = 0, class TW = Tw>
 __device__ __forceinline__ void fwd_lower_chain1(u32 *buf, u32 (&v)[16], int t,
-                                                 const ConvSmallParams &P, const Tw &W, Lay lay) {
+                                                 const ConvSmallParams &P, const TW &W, Lay lay) {
     if constexpr (I < Plan<K>::NP) {
         constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         constexpr int SB = Plan<K>::sb(I);
@@ -457,24 +486,24 @@ __device__ __forceinline__ void fwd_lower_chain1(u32 *buf, u32 (&v)[16], int t,
         __syncthreads();
         get<SB>(buf, v, t, lay);
         if (NT >= 16 || gblock_of_pass<K, I>(t) < NT)
-            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR>(v, t, P, W);
-        fwd_lower_chain1<K, I + 1, Lay, NT, AR>(buf, v, t, P, W, lay);
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v, t, P, W);
+        fwd_lower_chain1<K, I + 1, Lay, NT, AR, TW>(buf, v, t, P, W, lay);
     }
 }
 
-template <int K, int I, class Lay, int NT = 16, int AR = 0>
+template <int K, int I, class Lay, int NT = 16, int AR = 0, class TW = Tw>
 __device__ __forceinline__ void inv_lower_chain1(u32 *buf, u32 (&v)[16], int t,
-                                                 const ConvSmallParams &P, const Tw &W, Lay lay) {
+                                                 const ConvSmallParams &P, const TW &W, Lay lay) {
     if constexpr (I >= 0) {
         constexpr int SB = Plan<K>::sb(I);
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         if (NT >= 16 || gblock_of_pass<K, I>(t) < NT)
-            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR>(v, t, P, W);
+            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v, t, P, W);
         __syncthreads();
         put<SB>(buf, v, t, lay);
         __syncthreads();
         get<SBnext>(buf, v, t, lay);
-        inv_lower_chain1<K, I - 1, Lay, NT, AR>(buf, v, t, P, W, lay);
+        inv_lower_chain1<K, I - 1, Lay, NT, AR, TW>(buf, v, t, P, W, lay);
     }
 }
 

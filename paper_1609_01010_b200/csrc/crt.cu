@@ -2,35 +2,16 @@
 // the convolution engines (inputs reduced on load), then Garner CRT into
 // 3 x 32-bit limbs.  No reference counterpart; see
 // SURVEY.md section 8 a14 for the definition used here.
+#include <cstdlib>
 #include <cstring>
 
+#include "crt.cuh"
 #include "fourstep.cuh"
 #include "runtime.h"
 
 namespace mc {
 
-static const u32 kP[3] = {469762049u, 998244353u, 2013265921u};
-
-struct CrtConsts {
-    u32 p1, p2, p3;
-    Shoup inv12;     // p1^-1 mod p2
-    Shoup p1_mod3;   // p1 mod p3
-    Shoup inv123;    // (p1*p2)^-1 mod p3
-    unsigned long long p12;
-};
-
-static CrtConsts crt_consts() {
-    CrtConsts k;
-    k.p1 = kP[0];
-    k.p2 = kP[1];
-    k.p3 = kP[2];
-    k.inv12 = shoup(inv_mod(kP[0] % kP[1], kP[1]), kP[1]);
-    k.p1_mod3 = shoup(kP[0] % kP[2], kP[2]);
-    const u64 p12 = (u64)kP[0] * kP[1];
-    k.inv123 = shoup(inv_mod((u32)(p12 % kP[2]), kP[2]), kP[2]);
-    k.p12 = p12;
-    return k;
-}
+static const u32 kP[3] = {kCrtP1, kCrtP2, kCrtP3};
 
 // Garner: y2 = (r2 - r1) / p1 mod p2; x12 = r1 + p1*y2 (< p1*p2);
 // y3 = (r3 - x12) / (p1*p2) mod p3; x = x12 + p1*p2*y3 (< 2^90).
@@ -44,17 +25,11 @@ __global__ void crt3_kernel(const u32 *__restrict__ r1, const u32 *__restrict__ 
     for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (long long)gridDim.x * blockDim.x) {
         const u32 a = __ldcs(r1 + i), b = __ldcs(r2 + i), c = __ldcs(r3 + i);
-        const u32 y2 = mul_shoup(sub_mod(b, a, K.p2), K.inv12, K.p2);  // a < p1 < p2
-        const u32 x12m3 = add_mod(a, mul_shoup(y2, K.p1_mod3, K.p3), K.p3);
-        const u32 y3 = mul_shoup(sub_mod(c, x12m3, K.p3), K.inv123, K.p3);
-        const unsigned long long x12 = (unsigned long long)a + (unsigned long long)K.p1 * y2;
-        const unsigned long long lo = K.p12 * y3;
-        const unsigned long long hi = __umul64hi(K.p12, (unsigned long long)y3);
-        const unsigned long long s = lo + x12;
-        const unsigned long long h = hi + (s < lo ? 1ull : 0ull);
-        __stcs(limbs + i, (u32)s);
-        __stcs(limbs + ls + i, (u32)(s >> 32));
-        __stcs(limbs + 2 * ls + i, (u32)h);
+        u32 l0, l1, l2;
+        garner_limbs(a, garner_y2(a, b, K), c, K, l0, l1, l2);
+        __stcs(limbs + i, l0);
+        __stcs(limbs + ls + i, l1);
+        __stcs(limbs + 2 * ls + i, l2);
     }
 }
 
@@ -68,6 +43,18 @@ static mc_status launch_crt(const u32 *r1, const u32 *r2, const u32 *r3, u32 *li
     note_launches(1);
     MC_CUDA_CHECK(cudaGetLastError());
     return MC_OK;
+}
+
+// three_primes.cu: the fused four-step path (K = 18..23)
+bool three_primes_fused_ok(long long n);
+long long three_primes_fused_scratch(long long n);
+mc_status three_primes_fused(const u32 *a, int z1, const u32 *b, int z2, u32 *limbs,
+                             u32 *scratch, cudaStream_t st, cudaStream_t fs[3],
+                             cudaEvent_t fork_ev, cudaEvent_t done_ev[3]);
+
+static bool fused_on() {  // MC_NO_FUSED_CRT=1: per-prime products + crt3 (A/B)
+    static const bool on = [] { const char *e = getenv("MC_NO_FUSED_CRT"); return !(e && *e); }();
+    return on;
 }
 
 // product mod kP[k] of arbitrary-word inputs (reduced on load)
@@ -136,7 +123,9 @@ mc_status mc_copy_device(void *dst, const void *src, int64_t bytes, void *stream
 
 int64_t mc_three_primes_scratch_words(int32_t z1, int32_t z2) {
     if (z1 < 1 || z2 < 1) return 0;
-    return 3ll * ((int64_t)z1 + z2 - 1);
+    const long long n = (long long)z1 + z2 - 1;
+    if (fused_on() && three_primes_fused_ok(n)) return three_primes_fused_scratch(n);
+    return 3ll * n;
 }
 
 mc_status mc_mul_mod_prime_k(const uint32_t *a, int32_t z1, const uint32_t *b, int32_t z2,
@@ -167,6 +156,8 @@ mc_status mc_mul_three_primes(const uint32_t *a, int32_t z1, const uint32_t *b, 
         MC_CUDA_CHECK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
         dev_cached = dev;
     }
+    if (fused_on() && three_primes_fused_ok(n))
+        return three_primes_fused(a, z1, b, z2, limbs, scratch, st, fs, fork_ev, done_ev);
     uint32_t *res = scratch;
     bool own = false;
     if (!res) {

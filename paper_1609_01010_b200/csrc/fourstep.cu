@@ -12,13 +12,32 @@
 namespace mc {
 
 // ---------------------------------------------------------------- row kernel
+// The row transforms read one merged stage table (TwM: C - 1 + KC entries,
+// half of separate forward and inverse tables), which leaves room for three
+// 256-thread CTAs per SM at KC = 12 (80 registers, no spills).
+#ifndef MC_ROW_TM  // 0: separate forward / inverse stage tables in the row pass (A/B)
+#define MC_ROW_TM 1
+#endif
+#ifndef MC_ROW_MINB  // CTAs per SM of the 256-thread row pass (A/B: 3 measured slower)
+#define MC_ROW_MINB 2
+#endif
+#ifndef MC_ROW_STAGE  // stage the next row pair in shared memory by bulk copies (A/B)
+#define MC_ROW_STAGE 1
+#endif
+
 template <int KC>
 struct RowCfg {
     static constexpr int C = 1 << KC;
     static constexpr int T = C / 16;
     static constexpr int PPC = T >= 128 ? 1 : 128 / T;
     static constexpr int THREADS = T * PPC;
-    static constexpr int SMEM = 2 * C * 8 + PPC * (2 * C * 4 + 32 * 8);
+    static constexpr int TM = (C - 1 + KC + 1) & ~1;  // merged-table entries (even)
+    static constexpr int TABW = MC_ROW_TM ? TM : 2 * C;  // table entries in shared memory
+    // with one row pair per CTA (PPC == 1) the next pair lands in a staging
+    // area by bulk copies while the current one is transformed (TT path)
+    static constexpr bool STAGE = MC_ROW_STAGE && PPC == 1;
+    static constexpr int SMEM = TABW * 8 + PPC * (2 * C * 4 + 32 * 8) + (STAGE ? 2 * C * 4 + 16 : 0);
+    static constexpr int MINB = THREADS >= 512 ? 1 : THREADS == 256 ? MC_ROW_MINB : 2;
 };
 
 // AR: arithmetic mode (modarith.cuh); inputs and outputs in [0, 2p).
@@ -35,30 +54,56 @@ struct RowCfg {
 #endif
 
 template <int KC, int AR = 0, bool TT = false>
-__global__ void __launch_bounds__(RowCfg<KC>::THREADS, RowCfg<KC>::THREADS >= 512 ? 1 : 2)
+__global__ void __launch_bounds__(RowCfg<KC>::THREADS, RowCfg<KC>::MINB)
 row_conv_kernel(const FourParams P, int KR) {
     using RC = RowCfg<KC>;
     constexpr int Cn = RC::C, T = RC::T, G = Cn / 16;
     extern __shared__ uint4 smem_raw[];
-    uint2 *tf_s = reinterpret_cast<uint2 *>(smem_raw);
-    uint2 *ti_s = tf_s + Cn;
+    uint2 *tm_s = reinterpret_cast<uint2 *>(smem_raw);
     const int grp = threadIdx.x / T;
     const int t = threadIdx.x % T;
-    u32 *bufA = reinterpret_cast<u32 *>(ti_s + Cn) + grp * (2 * Cn + 64);
+    u32 *bufA = reinterpret_cast<u32 *>(tm_s + RC::TABW) + grp * (2 * Cn + 64);
     u32 *bufB = bufA + Cn;
     uint2 *beta = reinterpret_cast<uint2 *>(bufB + Cn);  // [0,16) fwd, [16,32) inv
+#if MC_ROW_TM
+    {
+        const uint4 *gm = reinterpret_cast<const uint4 *>(P.row_tm);
+        for (int i = threadIdx.x; i < RC::TM / 2; i += RC::THREADS)
+            reinterpret_cast<uint4 *>(tm_s)[i] = __ldg(gm + i);
+    }
+    const TwM W{tm_s};
+#else
     {
         const uint4 *gf = reinterpret_cast<const uint4 *>(P.row_tf);
         const uint4 *gi = reinterpret_cast<const uint4 *>(P.row_ti);
         for (int i = threadIdx.x; i < Cn / 2; i += RC::THREADS) {
-            reinterpret_cast<uint4 *>(tf_s)[i] = __ldg(gf + i);
-            reinterpret_cast<uint4 *>(ti_s)[i] = __ldg(gi + i);
+            reinterpret_cast<uint4 *>(tm_s)[i] = __ldg(gf + i);
+            reinterpret_cast<uint4 *>(tm_s + Cn)[i] = __ldg(gi + i);
         }
     }
-    const Tw W{tf_s, ti_s};
+    const Tw W{tm_s, tm_s + Cn};
+#endif
     const u32 p = P.cs.p;
     const long long R = 1ll << KR;
     const long long rows = P.nrows * P.chunk;  // truncated: only rows < nrows
+    // staging of the next row pair (TT path, PPC == 1): [a row][b row][mbarrier]
+    constexpr bool STG = TT && RC::STAGE;
+    u32 *stA = reinterpret_cast<u32 *>(tm_s + RC::TABW) + RC::PPC * (2 * Cn + 64);
+    u32 *stB = stA + Cn;
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(stB + Cn);
+    auto stage = [&](long long g) {  // thread 0: bulk copies of work item g's rows
+        const long long np = g % P.chunk, nr = g / P.chunk;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(mbar, 8u * Cn);
+        bulk_g2s(stA, P.Ah + np * (R << KC) + (nr << KC), 4u * Cn, mbar);
+        bulk_g2s(stB, P.Bh + np * (R << KC) + (nr << KC), 4u * Cn, mbar);
+    };
+    if (STG && threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        fence_mbar_init();
+        if ((long long)blockIdx.x < rows) stage(blockIdx.x);
+    }
+    uint32_t phase = 0;
     __syncthreads();
 
     for (long long base = (long long)blockIdx.x * RC::PPC; base < rows;
@@ -71,8 +116,10 @@ row_conv_kernel(const FourParams P, int KR) {
                 const long long ng = base + (long long)gridDim.x * RC::PPC;
                 if (ng < rows) {
                     const long long np = ng % P.chunk, nr = ng / P.chunk;
-                    bulk_prefetch_l2(P.Ah + np * (R << KC) + (nr << KC), 4u * Cn);
-                    bulk_prefetch_l2(P.Bh + np * (R << KC) + (nr << KC), 4u * Cn);
+                    if (!STG) {
+                        bulk_prefetch_l2(P.Ah + np * (R << KC) + (nr << KC), 4u * Cn);
+                        bulk_prefetch_l2(P.Bh + np * (R << KC) + (nr << KC), 4u * Cn);
+                    }
                     bulk_prefetch_l2(P.twf + (nr << KC), 8u * Cn);
                     bulk_prefetch_l2(P.twi + (nr << KC), 8u * Cn);
                 }
@@ -85,12 +132,27 @@ row_conv_kernel(const FourParams P, int KR) {
             const uint2 *twf = P.twf + (r << KC);
             const uint2 *twi = P.twi + (r << KC);
             u32 va[16], vb[16];
+            if constexpr (STG) {  // the row pair landed in the staging area
+                mbar_wait(mbar, phase);
+                phase ^= 1;
 #pragma unroll
-            for (int s = 0; s < 16; ++s) {
-                const int x = t + G * s;
-                const uint2 w = __ldg(twf + x);
-                va[s] = mul_t<AR>(valid ? rowA[x] : 0u, w.x, w.y, p);
-                vb[s] = mul_t<AR>(valid ? rowB[x] : 0u, w.x, w.y, p);
+                for (int s = 0; s < 16; ++s) {
+                    const int x = t + G * s;
+                    const uint2 w = __ldg(twf + x);
+                    va[s] = mul_t<AR>(stA[x], w.x, w.y, p);
+                    vb[s] = mul_t<AR>(stB[x], w.x, w.y, p);
+                }
+                __syncthreads();  // staging consumed: bring in the next work item's rows
+                const long long ng = base + (long long)gridDim.x;
+                if (threadIdx.x == 0 && ng < rows) stage(ng);
+            } else {
+#pragma unroll
+                for (int s = 0; s < 16; ++s) {
+                    const int x = t + G * s;
+                    const uint2 w = __ldg(twf + x);
+                    va[s] = mul_t<AR>(valid ? rowA[x] : 0u, w.x, w.y, p);
+                    vb[s] = mul_t<AR>(valid ? rowB[x] : 0u, w.x, w.y, p);
+                }
             }
             fwd_top<KC, 16, AR>(va, Cn, t, P.cs, W);
             fwd_top<KC, 16, AR>(vb, Cn, t, P.cs, W);
@@ -390,9 +452,9 @@ static cudaError_t launch_rows_any(int KC, int KR, const FourParams &P, cudaStre
     }
 }
 
-mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u32 *b,
+mc_status fourstep_plan(int engine, const u32 *a, long long lda, int z1, const u32 *b,
                         long long ldb, int z2, u32 *c, long long ldc, long long batch, u32 p,
-                        cudaStream_t st, int circ_log2L, bool reduce_inputs) {
+                        int circ_log2L, bool reduce_inputs, FourPlan *F) {
     const bool circ = circ_log2L >= 0;
     const long long n = circ ? (1ll << circ_log2L) : (long long)z1 + z2 - 1;
     int K = 0;
@@ -401,11 +463,11 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     const FieldTables *TL, *TR, *TC;
     mc_status s = get_tables(p, K, &TL);  // the reference's 2-adicity check
     if (s != MC_OK) return s;
-    if (K > kFourStepMaxK)  // L = 2^27 (p3 only): level-scheduled transforms
-        return levels_conv(a, lda, z1, b, ldb, z2, c, ldc, batch, p, K, n, st);
+    F->K = K;
+    if (K > kFourStepMaxK) return MC_OK;  // levels_conv territory (caller checks K)
     // Row length C = 2^KC: 2^12 (measured better than 2^13 at K = 23, whose
-    // wider column tiles do not pay for the 1-CTA/SM K=13 row pass);
-    // MC_FOURSTEP_KC overrides for A/B runs.
+    // wider column tiles do not pay for the 1-CTA/SM K=13 row pass, and than
+    // 2^11 at K = 21 and 23); MC_FOURSTEP_KC overrides for A/B runs.
     static const int kc_env = [] {
         const char *e = getenv("MC_FOURSTEP_KC");
         return e ? atoi(e) : 0;
@@ -418,7 +480,7 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     const int KR = K - KC;
     if ((s = get_tables(p, KR, &TR)) != MC_OK) return s;
     if ((s = get_tables(p, KC, &TC)) != MC_OK) return s;
-    FourParams P;
+    FourParams &P = F->P;
     memset(&P, 0, sizeof(P));
     if ((s = get_twist(TL, &P.tw)) != MC_OK) return s;
     if (twist_table_on(K) && (s = get_full_twist(TL, P.tw, KC, &P.twf, &P.twi)) != MC_OK)
@@ -447,6 +509,7 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     P.col_ti = TR->ti;
     P.row_tf = TC->tf;
     P.row_ti = TC->ti;
+    P.row_tm = TC->tm;
     const long long L = 1ll << K;
     // Truncation (tft engine): relaxed to L/16 granularity like the fused
     // kernel; the column transforms are truncated at NT of their 16 top
@@ -455,6 +518,47 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     if (engine == 1 && !circ) NT = (int)((n + (L >> 4) - 1) / (L >> 4));
     P.nrows = (long long)NT << (KR - 4);
     P.cs.ar = (NT == 16 && lazy_ok(p)) ? 1 : 2;
+    F->KC = KC;
+    F->KR = KR;
+    F->NT = NT;
+    F->L = L;
+    F->batch = batch;
+    F->tma = make_col_tma(a, lda, P.z1, b, ldb, P.z2, batch, KC, KR);
+    return MC_OK;
+}
+
+cudaError_t fourstep_fwd_rows(FourPlan &F, long long p0, int chunk, cudaStream_t st) {
+    FourParams &P = F.P;
+    P.prod0 = p0;
+    P.chunk = chunk;
+    // operand rows + twist tables of one chunk: prefetching pays once they
+    // cannot stay in the 126 MB L2 (config 4: -2.4%; config 5, 48 MB per
+    // prime: +1.3% without this gate)
+    P.row_prefetch = 8ll * F.L * P.chunk + 16ll * F.L > (96ll << 20) ? 1 : 0;
+    if (const char *f = getenv("MC_ROW_PREFETCH"))  // 0/1: force (sanitizer / A/B runs)
+        if (*f) P.row_prefetch = atoi(f) ? 1 : 0;
+    cudaError_t e = launch_cols_any(F.KC, F.KR, F.NT, P, true, st, &F.tma);
+    if (e == cudaSuccess) e = launch_rows_any(F.KC, F.KR, P, st);
+    note_launches(2);
+    return e;
+}
+
+cudaError_t fourstep_inv_cols(FourPlan &F, cudaStream_t st) {
+    note_launches(1);
+    return launch_cols_any(F.KC, F.KR, F.NT, F.P, false, st);
+}
+
+mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u32 *b,
+                        long long ldb, int z2, u32 *c, long long ldc, long long batch, u32 p,
+                        cudaStream_t st, int circ_log2L, bool reduce_inputs) {
+    FourPlan F;
+    mc_status s = fourstep_plan(engine, a, lda, z1, b, ldb, z2, c, ldc, batch, p, circ_log2L,
+                                reduce_inputs, &F);
+    if (s != MC_OK) return s;
+    if (F.K > kFourStepMaxK)  // L = 2^27 (p3 only): level-scheduled transforms
+        return levels_conv(a, lda, z1, b, ldb, z2, c, ldc, batch, p, F.K,
+                           circ_log2L >= 0 ? (1ll << circ_log2L) : (long long)z1 + z2 - 1, st);
+    const long long L = F.L;
     // scratch budget per chunk (default 512 MiB: bigger launches beat L2 residency,
     // the four-step passes are integer-pipe bound; profiles/r01/README.md)
     static const long long budget_words = [] {
@@ -465,23 +569,12 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
     u32 *scratch = nullptr;
     keep_pool_memory();
     MC_CUDA_CHECK(cudaMallocAsync(&scratch, sizeof(u32) * 2 * L * chunk, st));
-    P.Ah = scratch;
-    P.Bh = scratch + L * chunk;
-    const ColTma tma = make_col_tma(a, lda, P.z1, b, ldb, P.z2, batch, KC, KR);
+    F.P.Ah = scratch;
+    F.P.Bh = scratch + L * chunk;
     mc_status result = MC_OK;
     for (long long p0 = 0; p0 < batch && result == MC_OK; p0 += chunk) {
-        P.prod0 = p0;
-        P.chunk = (int)std::min(chunk, batch - p0);
-        // operand rows + twist tables of one chunk: prefetching pays once they
-        // cannot stay in the 126 MB L2 (config 4: -2.4%; config 5, 48 MB per
-        // prime: +1.3% without this gate)
-        P.row_prefetch = 8ll * L * P.chunk + 16ll * L > (96ll << 20) ? 1 : 0;
-        if (const char *f = getenv("MC_ROW_PREFETCH"))  // 0/1: force (sanitizer / A/B runs)
-            if (*f) P.row_prefetch = atoi(f) ? 1 : 0;
-        cudaError_t e = launch_cols_any(KC, KR, NT, P, true, st, &tma);
-        if (e == cudaSuccess) e = launch_rows_any(KC, KR, P, st);
-        if (e == cudaSuccess) e = launch_cols_any(KC, KR, NT, P, false, st);
-        note_launches(3);
+        cudaError_t e = fourstep_fwd_rows(F, p0, (int)std::min(chunk, batch - p0), st);
+        if (e == cudaSuccess) e = fourstep_inv_cols(F, st);
         if (e != cudaSuccess) result = cuda_fail(e, "four-step launch");
     }
     cudaFreeAsync(scratch, st);

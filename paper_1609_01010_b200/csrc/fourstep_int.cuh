@@ -35,6 +35,7 @@ struct FourParams {
     TwistTabs tw;
     const uint2 *col_tf, *col_ti;  // stage tables for the R-point column transforms
     const uint2 *row_tf, *row_ti;  // stage tables for the C-point row transforms
+    const uint2 *row_tm;           // merged stage table of the row transforms (TwM)
     long long nrows;  // rows of each product the row pass transforms (NT * R/16)
     // twist tables [R][C] (row_conv_kernel<.., TT = true>): twf[r][x] =
     // w_L^(x * rev(r)), twi[r][x] = w_L^-(x * rev(r)) * L^-1 * 2^32, Shoup pairs
@@ -106,6 +107,24 @@ cudaError_t launch_cols_kr12(const FourParams &P, int KC, int NT, bool fwd, cuda
                              const ColTma *tma = nullptr);
 cudaError_t launch_cols_kr13(const FourParams &P, int KC, int NT, bool fwd, cudaStream_t st,
                              const ColTma *tma = nullptr);
+
+// One four-step convolution set up for launching (fourstep.cu): tables,
+// twists and constants for one prime; the caller provides the scratch
+// (P.Ah, P.Bh: 2L words per product of a chunk).
+struct FourPlan {
+    FourParams P;
+    int K = 0, KC = 0, KR = 0, NT = 16;
+    long long L = 0, batch = 0;
+    ColTma tma;
+};
+
+mc_status fourstep_plan(int engine, const u32 *a, long long lda, int z1, const u32 *b,
+                        long long ldb, int z2, u32 *c, long long ldc, long long batch, u32 p,
+                        int circ_log2L, bool reduce_inputs, FourPlan *F);
+// forward column pass + fused row pass of products [p0, p0 + chunk)
+cudaError_t fourstep_fwd_rows(FourPlan &F, long long p0, int chunk, cudaStream_t st);
+// inverse column pass of the chunk last given to fourstep_fwd_rows
+cudaError_t fourstep_inv_cols(FourPlan &F, cudaStream_t st);
 
 template <class KF>
 static cudaError_t prep_kernel(KF kern, int smem, int threads, int *per_sm) {

@@ -178,6 +178,31 @@ __device__ __forceinline__ void bfly_dit_t(u32 &a, u32 &b, u32 w, u32 wp, u32 p)
     }
 }
 
+// DIT butterfly with the twiddle given NEGATED (w' = -w): the merged stage
+// table stores w_{2h}^{h-j} = -w_{2h}^{-j} for the inverse twiddles, so the
+// butterfly forms the same products and swaps its two outputs.
+template <int AR>
+__device__ __forceinline__ void bfly_dit_neg_t(u32 &a, u32 &b, u32 w, u32 wp, u32 p) {
+    if constexpr (MC_AR(AR) == 1) {  // [0, 4p) in and out
+        const u32 x = min(a, a - 2 * p);
+        const u32 t = mul_shoup_lazy(b, w, wp, p);
+        a = x - t + 2 * p;
+        b = x + t;
+    } else if constexpr (MC_AR(AR) == 2) {  // [0, 2p) in and out
+        const u32 x = min(a, a - p);
+        const u32 r = mul_shoup_lazy(b, w, wp, p);
+        const u32 t = min(r, r - p);
+        a = x - t + p;
+        b = x + t;
+    } else {
+        const u32 r = mul_shoup_lazy(b, w, wp, p);
+        const u32 t = min(r, r - p);
+        const u32 s = a + t, d = a - t + p;
+        a = min(d, d - p);
+        b = min(s, s - p);
+    }
+}
+
 // DIT butterfly with w = 1
 template <int AR>
 __device__ __forceinline__ void bfly_dit1_t(u32 &a, u32 &b, u32 p) {

@@ -251,14 +251,31 @@ mc_status get_tables(u32 p, int log2L, const FieldTables **out) {
         T->h16f[i] = hf[i];
         T->h16i[i] = hi[i];
     }
+    // merged table: L - 1 + log2 L entries, padded to a multiple of 2 (uint4 copies)
+    std::vector<uint2> hm;
+    for (u64 h = 1; h < L; h <<= 1) {
+        const u32 w = (u32)powmod(T->root, L / (2 * h), p);
+        u64 acc = 1;
+        for (u64 k = 0; k <= h; ++k) {
+            Shoup a = shoup((u32)acc, p);
+            hm.push_back(make_uint2(a.w, a.wp));
+            acc = mulmod(acc, w, p);
+        }
+    }
+    while (hm.size() % 2 || hm.size() < 2) hm.push_back(make_uint2(0, 0));
+    T->tm_entries = (int)hm.size();
     size_t bytes = sizeof(uint2) * hf.size();
     cudaError_t e = cudaMalloc(&T->tf, bytes);
     if (e == cudaSuccess) e = cudaMalloc(&T->ti, bytes);
     if (e == cudaSuccess) e = cudaMemcpy(T->tf, hf.data(), bytes, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(T->ti, hi.data(), bytes, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&T->tm, sizeof(uint2) * hm.size());
+    if (e == cudaSuccess)
+        e = cudaMemcpy(T->tm, hm.data(), sizeof(uint2) * hm.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) {
         cudaFree(T->tf);
         cudaFree(T->ti);
+        cudaFree(T->tm);
         delete T;
         return cuda_fail(e, "twiddle table upload");
     }

@@ -53,6 +53,10 @@ struct FieldTables {
     Shoup linv_mont;    // L^-1 * 2^32 mod p (undoes REDC's 2^-32)
     uint2 *tf = nullptr;
     uint2 *ti = nullptr;
+    // merged stage table (conv_small.cuh TwM): stage h = 2^lg at
+    // tm[h + lg - 1 + k] = w_{2h}^k, k = 0..h; tm_entries = its length
+    uint2 *tm = nullptr;
+    int tm_entries = 0;
     uint2 h16f[16] = {};  // host copies of tf[0..15] / ti[0..15]
     uint2 h16i[16] = {};
     Shoup mlev[5] = {};   // fused-kernel top-level constants (see ConvSmallParams)

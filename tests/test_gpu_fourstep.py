@@ -100,6 +100,25 @@ def test_cfg5_three_primes_pinned(golden_configs, orc):
             pin["per_prime"][str(p)]["sha256"], p
 
 
+@pytest.mark.parametrize("z1,z2", [(1 << 17, 1 << 17), (150001, 70001), (1 << 19, 1 << 18),
+                                   (262139, 262147), (1 << 22, 1 << 22)])
+def test_three_primes_fused_crt_path(orc, z1, z2):
+    """Four-step sizes K = 18..23 run the fused path (inverse column passes of
+    the three primes + Garner in one kernel): exact limbs vs the oracle,
+    including unaligned operand lengths (no tensor-map loads) and the
+    largest size p2's 2-adicity allows."""
+    rng = np.random.default_rng(z1 ^ (z2 << 1))
+    a = rng.integers(0, 1 << 30, z1, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, 1 << 30, z2, dtype=np.uint64).astype(np.uint32)
+    a[:5] = (1 << 30) - 1
+    b[-5:] = (1 << 30) - 1
+    at = torch.from_numpy(a.view(np.int32)).cuda()
+    bt = torch.from_numpy(b.view(np.int32)).cuda()
+    got = to_u32_np(mc.mul_three_primes_tensor(at, bt))
+    want = orc.mul_three_primes(a, b, threads=8)
+    assert np.array_equal(got, want), (z1, z2)
+
+
 @pytest.mark.parametrize("z1,z2", [(1, 1), (1, 9), (5, 3), (300, 200), (4096, 4096),
                                     (5000, 3), (20000, 17000)])
 def test_three_primes_small_exact(orc, z1, z2):
