@@ -455,6 +455,37 @@ __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[
     }
 }
 
+// Software-pipelined variant of fwd_lower_chain (MC_PIPE): the two operands'
+// exchanges are staggered so that every barrier interval mixes one operand's
+// shared-memory traffic with the other's butterflies, instead of running
+// both operands' exchanges back to back while the integer pipes idle.
+// Precondition: operand a's values for pass I are stored in bufA (not yet
+// ordered by a barrier); operand b's are in registers in the layout of the
+// previous pass.  Interval 1: get a, put b, pass I on a.  Interval 2: get b,
+// put a for pass I+1, pass I on b.
+template <int K, int NT, int I, int AR = 0, class TW = Tw>
+__device__ __forceinline__ void fwd_lower_pipe(u32 *bufA, u32 *bufB, u32 (&va)[16], u32 (&vb)[16],
+                                               int t, const ConvSmallParams &P, const TW &W) {
+    if constexpr (I < Plan<K>::NP) {
+        constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
+        constexpr int SB = Plan<K>::sb(I);
+        const bool act = pass_active<K, I, NT>(t);
+        __syncthreads();  // a's stores visible; every read of bufB done
+        get<SB>(bufA, va, t);
+        put<SBprev>(bufB, vb, t);
+        if (act) fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(va, t, P, W);
+        __syncthreads();  // b's stores visible; every read of bufA done
+        get<SB>(bufB, vb, t);
+        if constexpr (I + 1 < Plan<K>::NP) put<SB>(bufA, va, t);
+        if (act) fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(vb, t, P, W);
+        fwd_lower_pipe<K, NT, I + 1, AR, TW>(bufA, bufB, va, vb, t, P, W);
+    }
+}
+
+#ifndef MC_PIPE
+#define MC_PIPE 0  // measured: cfg2 +1%, cfg3 0% (the pipes, not the exchanges, bound the kernel)
+#endif
+
 // Inverse lower passes in reverse order (lowest bits first); on exit the
 // slots are in the top-pass layout.
 template <int K, int NT, int I, int AR = 0, class TW = Tw>
@@ -628,12 +659,25 @@ conv_small_kernel(const ConvSmallParams P) {
             }
         }
 
-        fwd_top<K, NT, AR, MC_PRESCALE != 0>(va, P.z1, t, P, W);
-        fwd_top<K, NT, AR>(vb, P.z2, t, P, W);
-        // the previous product's bulk store has read its staging before the
-        // first exchange (after the barrier inside the chain) reuses bufA
-        if ((FL & FL_HOST) && C::PPC == 1 && P.bulk_out && threadIdx.x == 0) bulk_wait_read_all();
-        fwd_lower_chain<K, NT, 0, AR>(bufA, bufB, va, vb, t, P, W);
+        if constexpr (MC_PIPE && Plan<K>::NP >= 1) {
+            fwd_top<K, NT, AR, MC_PRESCALE != 0>(va, P.z1, t, P, W);
+            // the previous product's bulk store has read its staging, and every
+            // thread is past its last read of bufA, before bufA is refilled
+            if ((FL & FL_HOST) && C::PPC == 1 && P.bulk_out && threadIdx.x == 0)
+                bulk_wait_read_all();
+            __syncthreads();
+            put<K - 4>(bufA, va, t);
+            fwd_top<K, NT, AR>(vb, P.z2, t, P, W);  // overlaps a's stores
+            fwd_lower_pipe<K, NT, 0, AR>(bufA, bufB, va, vb, t, P, W);
+        } else {
+            fwd_top<K, NT, AR, MC_PRESCALE != 0>(va, P.z1, t, P, W);
+            fwd_top<K, NT, AR>(vb, P.z2, t, P, W);
+            // the previous product's bulk store has read its staging before the
+            // first exchange (after the barrier inside the chain) reuses bufA
+            if ((FL & FL_HOST) && C::PPC == 1 && P.bulk_out && threadIdx.x == 0)
+                bulk_wait_read_all();
+            fwd_lower_chain<K, NT, 0, AR>(bufA, bufB, va, vb, t, P, W);
+        }
 
         // pointwise product in the last pass's layout, L^-1 folded in
         {
