@@ -85,6 +85,22 @@ static ConvSmallParams make_params(const FieldTables *T, const u32 *a, long long
     return P;
 }
 
+// TMA row prefetch of the fused kernel: one product per CTA, 16-byte aligned
+// rows, staging that fits in shared memory.
+static void setup_tma(ConvSmallParams &P, int K, bool allow) {
+    const bool one_per_cta = (1 << K) / 16 >= 128;
+    const bool aligned = ((uintptr_t)P.a % 16 == 0) && ((uintptr_t)P.b % 16 == 0) &&
+                         (P.lda % 4 == 0) && (P.ldb % 4 == 0);
+    const int za16 = P.z1 & ~3, zb16 = P.z2 & ~3;
+    const long long smem = 2ll * (1 << K) * 8 + 2ll * (1 << K) * 4 + 16 +
+                           4ll * (za16 + zb16);  // upper bound (tables in smem)
+    if (allow && one_per_cta && aligned && smem <= 227 * 1024 && P.batch > 0) {
+        P.tma = 1;
+        P.za16 = za16;
+        P.zb16 = zb16;
+    }
+}
+
 static cudaError_t launch_small(int K, const ConvSmallParams &P, int nt, cudaStream_t st) {
     switch (K) {
         case 4: return launch_conv_small_k4(P, nt, st);
@@ -108,6 +124,59 @@ struct StreamIn {
     uint32_t epoch;
     int rows;
 };
+
+// Split truncated product (tft engine just past a power of two): n = L/2 + m
+// with m <= L/8.  The relaxed truncated transform of the fused kernel keeps
+// whole 16ths of the transform and idles the warps of the skipped blocks, so
+// it gains little there (profiles/r01/sweep_fig3_*.csv).  Instead:
+//   head: c0 = c mod (x^(L/2) - 1), the complete half of the truncated
+//         transform, as an L/2-point cyclic convolution of the operands
+//         folded on load (a_x + a_{x+L/2});
+//   tail: low = the first m coefficients of a*b (operands truncated to m),
+//         then c[x] = low[x], c[L/2 + x] = c0[x] - low[x] for x < m.
+// Work ~ L/2 + 2m points instead of L; exact, so bit-identical to the
+// reference's tft x2 + pointwise + itft (convolve.py:230-253).
+static bool split_tft_on(int K, int n, long long batch) {
+    static const bool off = [] { const char *e = getenv("MC_NO_SPLIT_TFT"); return e && *e; }();
+    if (off || K < 5 || K > kSmallMaxK + 1) return false;
+    const int half = 1 << (K - 1), m = n - half;
+    if (m < 1 || m > (1 << K) / 8) return false;
+    // two launches: only where the kernels, not the launch latency, dominate
+    return K >= 10 || batch * (1ll << K) >= (1ll << 20);
+}
+
+static mc_status split_tft(const u32 *a, long long lda, int z1, const u32 *b, long long ldb,
+                           int z2, u32 *c, long long ldc, long long batch, u32 p, int K, int n,
+                           cudaStream_t st, bool allow_tma) {
+    if (z1 > z2) {  // the kernel folds L^-1 into operand a: make it the shorter one
+        std::swap(a, b);
+        std::swap(lda, ldb);
+        std::swap(z1, z2);
+    }
+    const int half = 1 << (K - 1), m = n - half;
+    const FieldTables *T1, *T2;
+    mc_status s = get_tables(p, K - 1, &T1);
+    if (s != MC_OK) return s;
+    ConvSmallParams H = make_params(T1, a, lda, z1, b, ldb, z2, c, ldc, half, batch);
+    H.fold = 1;
+    H.ar = lazy_ok(p) ? 1 : 2;
+    setup_tma(H, K - 1, allow_tma);
+    cudaError_t e = launch_small(K - 1, H, 16, st);
+    note_launches(1);
+    if (e != cudaSuccess) return cuda_fail(e, "split tft head launch");
+    const int y1 = std::min(z1, m), y2 = std::min(z2, m);
+    const int K2 = std::max(4, ceil_log2(y1 + y2 - 1));
+    if ((s = get_tables(p, K2, &T2)) != MC_OK) return s;
+    ConvSmallParams W = make_params(T2, a, lda, y1, b, ldb, y2, c, ldc, m, batch);
+    W.wrap_m = m;
+    W.wrap_off = half;
+    W.ar = lazy_ok(p) ? 1 : 2;
+    setup_tma(W, K2, allow_tma);
+    e = launch_small(K2, W, 16, st);
+    note_launches(1);
+    if (e != cudaSuccess) return cuda_fail(e, "split tft tail launch");
+    return MC_OK;
+}
 
 // engine 0 = fft_pad, 1 = tft; wrap != 0 => circular convolution of length L
 static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, const u32 *b,
@@ -135,6 +204,8 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
         MC_CUDA_CHECK(cudaGetLastError());
         return MC_OK;
     }
+    if (engine == 1 && !circ && !reduce && !host_out && !sin && split_tft_on(K, n, batch))
+        return split_tft(a, lda, z1, b, ldb, z2, c, ldc, batch, p, K, n, st, allow_tma);
     if (K <= kSmallMaxK) {
         if (z1 > z2) {  // the kernel folds L^-1 into operand a: make it the shorter one
             std::swap(a, b);
@@ -144,20 +215,7 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
         ConvSmallParams P = make_params(T, a, lda, z1, b, ldb, z2, c, ldc, n, batch);
         P.reduce = reduce ? 1 : 0;
         P.red_wp = (u32)((1ull << 32) / p);
-        // TMA row prefetch: one product per CTA, 16-byte aligned rows, fits in smem
-        {
-            const bool one_per_cta = (1 << K) / 16 >= 128;
-            const bool aligned = ((uintptr_t)a % 16 == 0) && ((uintptr_t)b % 16 == 0) &&
-                                 (lda % 4 == 0) && (ldb % 4 == 0);
-            const int za16 = z1 & ~3, zb16 = z2 & ~3;
-            const long long smem = 2ll * (1 << K) * 8 + 2ll * (1 << K) * 4 + 16 +
-                                   4ll * (za16 + zb16);  // upper bound (tables in smem)
-            if (allow_tma && one_per_cta && aligned && smem <= 227 * 1024 && batch > 0) {
-                P.tma = 1;
-                P.za16 = za16;
-                P.zb16 = zb16;
-            }
-        }
+        setup_tma(P, K, allow_tma);
         if (sin) {  // streamed inputs: only the bulk-copy prefetch can wait for them
             if (!P.tma) return fail(MC_EINVAL, "streamed inputs need the bulk-copy path");
             P.ready = sin->flags;
@@ -168,6 +226,9 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
         if (engine == 1 && !circ) {
             const int G = 1 << (K - 4);
             nt = (n + G - 1) / G;
+            // relaxation: NT = 15 saves 1/16 of the work, less than the lazy
+            // (Harvey) arithmetic of the complete transform gains for p < 2^30
+            if (nt == 15 && lazy_ok(p)) nt = 16;
         }
         if (batch > 0x7fffffffll * SmallCfg<4>::PPC)
             return fail(MC_EINVAL, "batch too large for one launch");

@@ -71,6 +71,13 @@ struct ConvSmallParams {
     const uint32_t *ready;  // streamed inputs (PPC == 1 with TMA): rows of chunk i are
     uint32_t epoch;         // resident once ready[i] == epoch (set by the copy stream)
     int ready_rows;         // products per chunk
+    // Split truncated product (tft engine, n = L/2 + m with m <= L/8; capi.cu
+    // conv_dispatch): the head launch (fold) forms c mod (x^(L/2) - 1) from
+    // operands folded on load, the tail launch (wrap_m = m) forms the low
+    // product and unwraps: c[x] = low[x], c[wrap_off + x] = c0[x] - low[x].
+    int fold;      // FL_FOLD launch: rows longer than L fold x + L onto x
+    int wrap_m;    // FL_WRAP launch: coefficients to unwrap (== n)
+    int wrap_off;  // FL_WRAP launch: half length of the full product transform
 };
 
 // Shared-memory swizzle of the exchanges: XOR of position bits [2,5) with
@@ -558,6 +565,8 @@ struct SmallCfg {
 // registers and scheduling freedom in the butterfly stream.
 constexpr int FL_HOST = 1;    // bulk-store epilogue / streamed-input ready flags (zero copy)
 constexpr int FL_REDUCE = 2;  // operands are arbitrary words: reduce mod p on load
+constexpr int FL_FOLD = 4;    // split truncated product, head: fold rows longer than L
+constexpr int FL_WRAP = 8;    // split truncated product, tail: unwrap the head's result
 
 // Persistent kernel: each CTA copies the (p, L) stage tables into shared
 // memory once and then walks the batch with a grid stride.
@@ -631,6 +640,10 @@ conv_small_kernel(const ConvSmallParams P) {
                 const int x = (s << (K - 4)) | t;
                 va[s] = x < P.za16 ? stA[x] : 0u;
                 vb[s] = x < P.zb16 ? stB[x] : 0u;
+                if constexpr ((FL & FL_FOLD) != 0) {  // x + L wraps onto x mod (x^L - 1)
+                    if (x + L < P.za16) va[s] = add_mod(va[s], stA[x + L], P.p);
+                    if (x + L < P.zb16) vb[s] = add_mod(vb[s], stB[x + L], P.p);
+                }
             }
             if (P.z1 != P.za16 || P.z2 != P.zb16) {  // uniform: rows not a multiple of 4
 #pragma unroll
@@ -638,6 +651,11 @@ conv_small_kernel(const ConvSmallParams P) {
                     const int x = (s << (K - 4)) | t;
                     if (x >= P.za16 && x < P.z1) va[s] = __ldcs(ga + x);
                     if (x >= P.zb16 && x < P.z2) vb[s] = __ldcs(gb + x);
+                    if constexpr ((FL & FL_FOLD) != 0) {
+                        const int y = x + L;
+                        if (y >= P.za16 && y < P.z1) va[s] = add_mod(va[s], __ldcs(ga + y), P.p);
+                        if (y >= P.zb16 && y < P.z2) vb[s] = add_mod(vb[s], __ldcs(gb + y), P.p);
+                    }
                 }
             }
             __syncthreads();  // staging consumed: refill it for the next product
@@ -649,6 +667,10 @@ conv_small_kernel(const ConvSmallParams P) {
                 const int x = (s << (K - 4)) | t;
                 va[s] = (valid && x < P.z1) ? __ldcs(ga + x) : 0u;
                 vb[s] = (valid && x < P.z2) ? __ldcs(gb + x) : 0u;
+                if constexpr ((FL & FL_FOLD) != 0) {
+                    if (valid && x + L < P.z1) va[s] = add_mod(va[s], __ldcs(ga + x + L), P.p);
+                    if (valid && x + L < P.z2) vb[s] = add_mod(vb[s], __ldcs(gb + x + L), P.p);
+                }
             }
         }
         if ((FL & FL_REDUCE) && P.reduce) {  // three-primes inputs: any 32-bit word -> residue
@@ -736,10 +758,30 @@ conv_small_kernel(const ConvSmallParams P) {
             if (head + nb + t < P.n) gc[head + nb + t] = stg[head + nb + t];
         } else if (valid) {
             u32 *gc = P.c + row * P.ldc;
+            if constexpr ((FL & FL_WRAP) != 0) {
+                // c0 = c mod (x^(L/2) - 1) from the head launch holds c[x] +
+                // c[x + L/2] for x < m; the low product gives c[x]
+                u32 c0[16];  // all loads in flight before the first store
 #pragma unroll
-            for (int s = 0; s < 16; ++s) {
-                const int x = (s << (K - 4)) | t;
-                if (x < P.n) __stcs(gc + x, canon_t<AR>(va[s], P.p));
+                for (int s = 0; s < 16; ++s) {
+                    const int x = (s << (K - 4)) | t;
+                    c0[s] = x < P.wrap_m ? __ldcs(gc + x) : 0u;
+                }
+#pragma unroll
+                for (int s = 0; s < 16; ++s) {
+                    const int x = (s << (K - 4)) | t;
+                    if (x < P.wrap_m) {
+                        const u32 lo = canon_t<AR>(va[s], P.p);
+                        __stcs(gc + x, lo);
+                        __stcs(gc + P.wrap_off + x, sub_mod(c0[s], lo, P.p));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int s = 0; s < 16; ++s) {
+                    const int x = (s << (K - 4)) | t;
+                    if (x < P.n) __stcs(gc + x, canon_t<AR>(va[s], P.p));
+                }
             }
         }
     }

@@ -44,6 +44,16 @@ static cudaError_t launch_nt_fl(const ConvSmallParams &P, cudaStream_t st) {
 template <int NT, int AR>
 static cudaError_t launch_nt(const ConvSmallParams &P, cudaStream_t st) {
     constexpr bool one_per_cta = SmallCfg<MC_K>::PPC == 1;
+    if (P.fold || P.wrap_m) {  // split truncated product: complete transforms, device rows
+        if constexpr (NT == 16) {
+            if (P.reduce || P.bulk_out || P.ready || (P.fold && P.wrap_m))
+                return cudaErrorInvalidValue;
+            return P.fold ? launch_nt_fl<NT, AR, FL_FOLD>(P, st)
+                          : launch_nt_fl<NT, AR, FL_WRAP>(P, st);
+        } else {
+            return cudaErrorInvalidValue;
+        }
+    }
     if (P.reduce) {
         if constexpr (NT == 16) {
             if (P.bulk_out || P.ready) return cudaErrorInvalidValue;

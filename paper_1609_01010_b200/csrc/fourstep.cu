@@ -516,6 +516,7 @@ mc_status fourstep_plan(int engine, const u32 *a, long long lda, int z1, const u
     // blocks and the row pass only forms rows < NT * R/16.
     int NT = 16;
     if (engine == 1 && !circ) NT = (int)((n + (L >> 4) - 1) / (L >> 4));
+    if (NT == 15 && lazy_ok(p)) NT = 16;  // as the fused path (capi.cu conv_dispatch)
     P.nrows = (long long)NT << (KR - 4);
     P.cs.ar = (NT == 16 && lazy_ok(p)) ? 1 : 2;
     F->KC = KC;

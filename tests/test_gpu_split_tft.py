@@ -1,0 +1,109 @@
+"""Split truncated product (tft engine, n = L/2 + m with m <= L/8): a cyclic
+L/2-point head on operands folded on load plus a low-product tail that
+unwraps the top m coefficients (capi.cu split_tft).  Bit-exact against the C
+oracle's conv_tft (reference convolve.py:230-253) over every K where the
+split applies, the m boundaries, balanced and lopsided operand lengths,
+strided rows (plain loads) and aligned rows (bulk-copy staging), and the
+all-(p-1) operands."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import P1, P2, P3
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_1609_01010_b200 as mc
+    from paper_1609_01010_b200 import _native
+    from gpu_helpers import to_u32_np
+
+
+def _dev(x, ld=None):
+    x = np.ascontiguousarray(x, dtype=np.uint32)
+    if ld is None:
+        return torch.from_numpy(x.view(np.int32)).cuda()
+    buf = torch.zeros((x.shape[0], ld), dtype=torch.int32, device="cuda")
+    buf[:, : x.shape[1]] = torch.from_numpy(x.view(np.int32)).cuda()
+    return buf[:, : x.shape[1]]
+
+
+def _rows(K):
+    # below K = 10 the split is taken only for batches of >= 2^20 positions
+    return 3 if K >= 10 else (1 << 20) >> K
+
+
+def _check(orc, p, z1, z2, rows, seed, ld=None):
+    a = orc.gen_u32(seed, 0, z1, rows, z1, p)
+    b = orc.gen_u32(seed, 1, z2, rows, z2, p)
+    want, _, _ = orc.conv_batch(a, b, p, orc.ENGINE_TFT)
+    before = _native.launch_count()
+    got = to_u32_np(mc.conv_batch(_dev(a, ld), _dev(b, ld), p, engine="tft"))
+    launches = _native.launch_count() - before
+    assert np.array_equal(got, want), (p, z1, z2, rows, np.argwhere(got != want)[:4].tolist())
+    return launches
+
+
+@pytest.mark.parametrize("K", list(range(5, 15)))
+def test_split_boundaries(orc, K):
+    L = 1 << K
+    for m in sorted({1, 2, 3, 7, L // 16 - 1, L // 16, L // 16 + 1, L // 8 - 1, L // 8}):
+        if m < 1 or m > L // 8:
+            continue
+        n = L // 2 + m
+        for z1 in sorted({1, 2, (n + 1) // 2, m, L // 2, L // 2 + 1}):
+            z2 = n + 1 - z1
+            if z1 < 1 or z2 < 1:
+                continue
+            launches = _check(orc, P3, z1, z2, _rows(K), seed=K * 1000 + m)
+            assert launches == 2, (K, m, z1, launches)  # the head and the tail
+
+
+@pytest.mark.parametrize("p", [P1, P2, P3])
+def test_split_strided_and_aligned(orc, p):
+    for K in (11, 12, 13, 14):
+        L = 1 << K
+        for m in (5, L // 8):
+            n = L // 2 + m
+            z1 = (n + 1) // 2
+            z2 = n + 1 - z1
+            _check(orc, p, z1, z2, 4, seed=7 + K, ld=z2 + 5)    # odd stride: plain loads
+            _check(orc, p, z1, z2, 4, seed=9 + K, ld=((z2 + 3) // 4) * 4 + 4)  # bulk copies
+
+
+def test_split_all_p_minus_1(orc):
+    for K in (8, 12, 14):
+        L = 1 << K
+        for m in (1, L // 8):
+            n = L // 2 + m
+            z1 = (n + 1) // 2
+            z2 = n + 1 - z1
+            rows = _rows(K)
+            a = np.full((rows, z1), P3 - 1, dtype=np.uint32)
+            b = np.full((rows, z2), P3 - 1, dtype=np.uint32)
+            want, _, _ = orc.conv_batch(a[:1], b[:1], P3, orc.ENGINE_TFT)
+            got = to_u32_np(mc.conv_batch(_dev(a), _dev(b), P3, engine="tft"))
+            assert np.array_equal(got, np.repeat(want, rows, axis=0)), (K, m)
+
+
+def test_split_not_taken_past_eighth(orc):
+    """m > L/8 keeps the single relaxed-truncation launch."""
+    L = 4096
+    n = L // 2 + L // 8 + 1
+    z1 = (n + 1) // 2
+    assert _check(orc, P2, z1, n + 1 - z1, 3, seed=5) == 1
+
+
+def test_split_poly_mul_counters():
+    """poly_mul through the split path: normalized result and the
+    reference's analytic TFT counters (convolve.py:230-253)."""
+    fp = mc.FourierPrime.from_modulus(P2)
+    rng = np.random.default_rng(3)
+    a = mc.DensePoly(fp, tuple(int(x) for x in rng.integers(0, P2, 1030)))
+    b = mc.DensePoly(fp, tuple(int(x) for x in rng.integers(0, P2, 1031)))
+    cnt = mc.OpCounters()
+    r = mc.poly_mul(a, b, mc.ConvRequest(fp, engine="tft", counters=cnt))
+    r2 = mc.poly_mul(a, b, mc.ConvRequest(fp, engine="fft_pad"))
+    assert r == r2 and len(r.coeffs) == 2060
+    assert cnt.butterflies > 0
