@@ -369,6 +369,7 @@ struct LayCol {
 
 template <int SB, class Lay = LaySmall>
 __device__ __forceinline__ void put(u32 *buf, const u32 (&v)[16], int t, Lay lay = Lay()) {
+    mc_perturb();
     if constexpr (SB == 0 && std::is_same<Lay, LaySmall>::value) {
 #pragma unroll
         for (int k = 0; k < 4; ++k)  // positions 16t + 4k .. +3: one aligned quad
@@ -382,6 +383,7 @@ __device__ __forceinline__ void put(u32 *buf, const u32 (&v)[16], int t, Lay lay
 
 template <int SB, class Lay = LaySmall>
 __device__ __forceinline__ void get(const u32 *buf, u32 (&v)[16], int t, Lay lay = Lay()) {
+    mc_perturb();
     if constexpr (SB == 0 && std::is_same<Lay, LaySmall>::value) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -446,10 +448,12 @@ __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[
     if constexpr (I < Plan<K>::NP) {
         constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         constexpr int SB = Plan<K>::sb(I);
-        __syncthreads();
+        mc_sync();
         put<SBprev>(bufA, va, t);
         put<SBprev>(bufB, vb, t);
-        __syncthreads();
+#ifndef MC_RACE_SELFTEST  // self-test of the race-stress build: this barrier removed must fail
+        mc_sync();
+#endif
         get<SB>(bufA, va, t);
         get<SB>(bufB, vb, t);
         // Inactive G-blocks (>= NT) are skipped per warp where possible;
@@ -477,11 +481,11 @@ __device__ __forceinline__ void fwd_lower_pipe(u32 *bufA, u32 *bufB, u32 (&va)[1
         constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         constexpr int SB = Plan<K>::sb(I);
         const bool act = pass_active<K, I, NT>(t);
-        __syncthreads();  // a's stores visible; every read of bufB done
+        mc_sync();  // a's stores visible; every read of bufB done
         get<SB>(bufA, va, t);
         put<SBprev>(bufB, vb, t);
         if (act) fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(va, t, P, W);
-        __syncthreads();  // b's stores visible; every read of bufA done
+        mc_sync();  // b's stores visible; every read of bufA done
         get<SB>(bufB, vb, t);
         if constexpr (I + 1 < Plan<K>::NP) put<SB>(bufA, va, t);
         if (act) fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(vb, t, P, W);
@@ -503,9 +507,9 @@ __device__ __forceinline__ void inv_lower_chain(u32 *buf, u32 (&v)[16], int t,
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         if (pass_active<K, I, NT>(t))
             inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v, t, P, W);  // zeros stay zeros
-        __syncthreads();
+        mc_sync();
         put<SB>(buf, v, t);
-        __syncthreads();
+        mc_sync();
         get<SBnext>(buf, v, t);
         inv_lower_chain<K, NT, I - 1, AR, TW>(buf, v, t, P, W);
     }
@@ -519,9 +523,9 @@ __device__ __forceinline__ void fwd_lower_chain1(u32 *buf, u32 (&v)[16], int t,
     if constexpr (I < Plan<K>::NP) {
         constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         constexpr int SB = Plan<K>::sb(I);
-        __syncthreads();
+        mc_sync();
         put<SBprev>(buf, v, t, lay);
-        __syncthreads();
+        mc_sync();
         get<SB>(buf, v, t, lay);
         if (NT >= 16 || gblock_of_pass<K, I>(t) < NT)
             fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v, t, P, W);
@@ -537,9 +541,9 @@ __device__ __forceinline__ void inv_lower_chain1(u32 *buf, u32 (&v)[16], int t,
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         if (NT >= 16 || gblock_of_pass<K, I>(t) < NT)
             inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v, t, P, W);
-        __syncthreads();
+        mc_sync();
         put<SB>(buf, v, t, lay);
-        __syncthreads();
+        mc_sync();
         get<SBnext>(buf, v, t, lay);
         inv_lower_chain1<K, I - 1, Lay, NT, AR, TW>(buf, v, t, P, W, lay);
     }
@@ -622,7 +626,7 @@ conv_small_kernel(const ConvSmallParams P) {
         bulk_g2s(tf_s, P.tf, L * 8u, mbar);
         bulk_g2s(ti_s, P.ti, L * 8u, mbar);
     }
-    __syncthreads();
+    mc_sync();
     uint32_t phase = 0;
 
     for (long long base = (long long)blockIdx.x * C::PPC; base < P.batch;
@@ -658,7 +662,7 @@ conv_small_kernel(const ConvSmallParams P) {
                     }
                 }
             }
-            __syncthreads();  // staging consumed: refill it for the next product
+            mc_sync();  // staging consumed: refill it for the next product
             const long long nxt = base + (long long)gridDim.x * C::PPC;
             if (threadIdx.x == 0 && nxt < P.batch) prefetch(nxt, 0u);
         } else {
@@ -687,7 +691,7 @@ conv_small_kernel(const ConvSmallParams P) {
             // thread is past its last read of bufA, before bufA is refilled
             if ((FL & FL_HOST) && C::PPC == 1 && P.bulk_out && threadIdx.x == 0)
                 bulk_wait_read_all();
-            __syncthreads();
+            mc_sync();
             put<K - 4>(bufA, va, t);
             fwd_top<K, NT, AR>(vb, P.z2, t, P, W);  // overlaps a's stores
             fwd_lower_pipe<K, NT, 0, AR>(bufA, bufB, va, vb, t, P, W);
@@ -742,12 +746,12 @@ conv_small_kernel(const ConvSmallParams P) {
             u32 *gc = P.c + row * P.ldc;
             const int mis = (int)(((uintptr_t)gc >> 2) & 3);
             u32 *stg = bufA + mis;
-            __syncthreads();  // every thread is done reading bufA
+            mc_sync();  // every thread is done reading bufA
 #pragma unroll
             for (int s = 0; s < 16; ++s)
                 stg[(s << (K - 4)) | t] = canon_t<AR>(va[s], P.p);
             fence_proxy_async_smem();
-            __syncthreads();
+            mc_sync();
             const int head = min((4 - mis) & 3, P.n);
             const int nb = ((P.n - head) >> 2) << 2;  // words in the bulk part
             if (threadIdx.x == 0 && nb > 0) {

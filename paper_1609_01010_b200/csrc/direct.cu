@@ -14,6 +14,7 @@
 // accumulated exactly as two 64-bit sums of their low and high words
 // (IMAD + IMAD.HI + two 64-bit adds) and reduced once at the end.
 #include "runtime.h"
+#include "tma.cuh"
 
 namespace mc {
 
@@ -35,7 +36,7 @@ __global__ void __launch_bounds__(kDirTile) direct_conv_kernel(
     }
     unsigned long long s_lo = 0, s_hi = 0;
     for (int i0 = i_lo; i0 < i_hi; i0 += kDirTile) {
-        __syncthreads();
+        mc_sync();
         sa[t] = (i0 + t < i_hi) ? ar[i0 + t] : 0u;
         // sb[x] = b[k0 - i0 - (kDirTile - 1) + x]: output k = k0 + t and a index
         // i0 + ii meet b[k - i0 - ii] = sb[t - ii + kDirTile - 1]
@@ -51,7 +52,7 @@ __global__ void __launch_bounds__(kDirTile) direct_conv_kernel(
             }
             sb[x] = w;
         }
-        __syncthreads();
+        mc_sync();
 #pragma unroll 8
         for (int ii = 0; ii < kDirTile; ++ii) {
             const u32 x = sa[ii], y = sb[t - ii + kDirTile - 1];

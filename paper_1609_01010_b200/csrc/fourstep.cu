@@ -104,7 +104,7 @@ row_conv_kernel(const FourParams P, int KR) {
         if ((long long)blockIdx.x < rows) stage(blockIdx.x);
     }
     uint32_t phase = 0;
-    __syncthreads();
+    mc_sync();
 
     for (long long base = (long long)blockIdx.x * RC::PPC; base < rows;
          base += (long long)gridDim.x * RC::PPC) {
@@ -142,7 +142,7 @@ row_conv_kernel(const FourParams P, int KR) {
                     va[s] = mul_t<AR>(stA[x], w.x, w.y, p);
                     vb[s] = mul_t<AR>(stB[x], w.x, w.y, p);
                 }
-                __syncthreads();  // staging consumed: bring in the next work item's rows
+                mc_sync();  // staging consumed: bring in the next work item's rows
                 const long long ng = base + (long long)gridDim.x;
                 if (threadIdx.x == 0 && ng < rows) stage(ng);
             } else {
@@ -169,7 +169,7 @@ row_conv_kernel(const FourParams P, int KR) {
                     rowA[x] = mul_inv_t<AR>(va[s], w.x, w.y, p);
                 }
             }
-            __syncthreads();
+            mc_sync();
             continue;
         }
         const long long prod = valid ? gr / P.nrows : 0;
@@ -190,7 +190,7 @@ row_conv_kernel(const FourParams P, int KR) {
         const u32 aip = shoup_comp(ai, p, P.tw.two32_over_p);
         u32 *rowA = P.Ah + prod * (R << KC) + ((long long)r << KC);
         const u32 *rowB = P.Bh + prod * (R << KC) + ((long long)r << KC);
-        __syncthreads();
+        mc_sync();
 
         u32 va[16], vb[16];
 #pragma unroll
@@ -215,7 +215,7 @@ row_conv_kernel(const FourParams P, int KR) {
                 rowA[t + G * s] = mul_inv_t<AR>(mul_inv_t<AR>(va[s], ai, aip, p), bt.x, bt.y, p);
             }
         }
-        __syncthreads();
+        mc_sync();
     }
 }
 

@@ -34,7 +34,7 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_fwd
     const int t = threadIdx.x / C::TC;
     const long long col = (long long)blockIdx.x * C::TC + c;
     const u32 p = P.cs.p;
-    __syncthreads();
+    mc_sync();
 
     u32 v[16];
 #pragma unroll
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_inv
     const int c = threadIdx.x % C::TC;
     const int t = threadIdx.x / C::TC;
     const long long col = (long long)blockIdx.x * C::TC + c;
-    __syncthreads();
+    mc_sync();
 
     u32 v[16];
     constexpr int SB = last_sb<KR>();
@@ -146,7 +146,7 @@ col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
         mbar_init(bar + 1, 1);
         fence_mbar_init();
     }
-    __syncthreads();
+    mc_sync();
     auto issue = [&](int tile, int k) {  // thread 0
         const int ct = tile % CT, op = (tile / CT) & 1, pc = tile / (2 * CT);
         u32 *dst = k ? buf1 : buf0;
@@ -177,7 +177,7 @@ col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
             if (P.reduce) x = mul_t<AR>(x, 1u, P.red_wp, p);
             v[s] = x;
         }
-        __syncthreads();  // tile consumed; the other buffer is free since last iteration
+        mc_sync();  // tile consumed; the other buffer is free since last iteration
         if (threadIdx.x == 0 && tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, k ^ 1);
         const long long z = op ? P.z2 : P.z1;
         const int zrows = (int)((z + Ccols - 1) / Ccols);
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(1024, 1) col_inv_async_kernel(const FourParams
         const int ct = tile % CT, pc = tile / CT;
         u32 *buf = bufs + k * A::BUFW;
         asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
+        mc_sync();
         u32 v[16];
         constexpr int SB = last_sb<KR>();
 #pragma unroll
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(1024, 1) col_inv_async_kernel(const FourParams
             const int row = slot_pos<SB>(t, s);
             v[s] = (NT >= 16 || (row >> (KR - 4)) < NT) ? buf[A::off(row) + c] : 0u;
         }
-        __syncthreads();  // tile consumed; the other buffer is free
+        mc_sync();  // tile consumed; the other buffer is free
         if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, k ^ 1);
         LayCol<C::TC> lay{c};
         inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, NT, AR>(buf, v, t, P.cs, W, lay);

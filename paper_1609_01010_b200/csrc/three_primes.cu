@@ -105,7 +105,7 @@ col_inv3_crt_kernel(const Inv3Params Q, int ntiles) {
     // the next step's copy may be queued into it.
     auto land = [&]() {
         asm volatile("cp.async.wait_group 0;" ::: "memory");
-        __syncthreads();
+        mc_sync();
     };
     if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0, 0);
     int sel = 0;  // three steps per tile over two buffers: the parity alternates

@@ -4,6 +4,31 @@
 #pragma once
 #include <cstdint>
 
+// Race-stress builds (-DMC_RACE_CHECK; scripts/gpu_race_check.sh).  The
+// pool's compute-sanitizer is closed, so synchronisation is checked by
+// perturbation instead: after every CTA barrier and mbarrier wait, and before
+// every shared-memory exchange, a pseudo-random eighth of the threads sleeps
+// up to ~2 us.  A missing barrier, a buffer refilled while still being read,
+// or an exchange read before its write then reads data of another stage and
+// the bit-exact parity tests fail.  Normal builds compile this to nothing.
+#ifdef MC_RACE_CHECK
+__device__ __forceinline__ void mc_perturb() {
+    unsigned h = (threadIdx.x + 1u) * 2654435761u ^ (blockIdx.x + 7u) * 40503u ^
+                 (unsigned)clock();
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    h ^= h >> 15;
+    if ((h & 7u) == 0u) __nanosleep((h >> 8) & 2047u);
+}
+#else
+__device__ __forceinline__ void mc_perturb() {}
+#endif
+
+__device__ __forceinline__ void mc_sync() {
+    __syncthreads();
+    mc_perturb();
+}
+
 namespace mc {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -50,6 +75,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "}\n" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+    mc_perturb();
 }
 
 // 3-D tensor tile load (cp.async.bulk.tensor, SASS UTMALDG): box at

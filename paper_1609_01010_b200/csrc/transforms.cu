@@ -358,9 +358,9 @@ __global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
     for (long long r = blockIdx.x; r < P.batch; r += gridDim.x) {
         const u32 *xr = P.x + r * P.ldx;
         const int zin = MODE == 0 ? P.z : n;
-        __syncthreads();  // the previous row's stores have read s
+        mc_sync();  // the previous row's stores have read s
         for (int i = tid; i < L; i += NTH) s[i] = i < zin ? mul_shoup(__ldcs(xr + i), 1u, P.red_wp, p) : 0u;
-        __syncthreads();
+        mc_sync();
         if (MODE == 0) {
             for (int h = L >> 1; h >= 1; h >>= 1) {
                 const int m = 2 * h, lgh = __ffs(h) - 1;
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
                         s[lo] = add_mod(s[lo], s[hi], p);
                     }
                 }
-                __syncthreads();
+                mc_sync();
             }
         } else {
             // 1. complete blocks: inverse DIT, stage h over the aligned 2h-chunks
@@ -419,10 +419,10 @@ __global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
                             s[lo] = add_mod(a, t, p);
                             s[hi] = sub_mod(a, t, p);
                         }
-                        __syncthreads();
+                        mc_sync();
                     }
                 }
-                __syncthreads();
+                mc_sync();
                 h <<= nb;
             }
             // 2./3. the partial path: down (cross butterflies where n > h, else
@@ -465,24 +465,26 @@ __global__ void __launch_bounds__(512) rows_kernel(const RowsParams P) {
             };
             for (int c = 0; c < P.nbig; ++c) {
                 node_down(c, tid, NTH);
-                __syncthreads();
+                mc_sync();
             }
             if (P.nbig < P.nc) {
                 if (tid < 32) {
                     for (int c = P.nbig; c < P.nc; ++c) {
                         node_down(c, tid, 32);
                         __syncwarp();
+                        mc_perturb();
                     }
                     for (int c = P.nc - 1; c >= P.nbig; --c) {
                         node_up(c, tid, 32);
                         __syncwarp();
+                        mc_perturb();
                     }
                 }
-                __syncthreads();
+                mc_sync();
             }
             for (int c = P.nbig - 1; c >= 0; --c) {
                 node_up(c, tid, NTH);
-                __syncthreads();
+                mc_sync();
             }
         }
         u32 *yr = P.y + r * P.ldy;

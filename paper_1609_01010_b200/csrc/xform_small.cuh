@@ -51,7 +51,7 @@ xform_small_kernel(const XformParams X) {
     const int t = threadIdx.x % T;
     u32 *buf = data + grp * L;
     const u32 p = X.cs.p;
-    __syncthreads();
+    mc_sync();
     constexpr int SBL = last_sb<K>();
     for (long long base = (long long)blockIdx.x * C::PPC; base < X.batch;
          base += (long long)gridDim.x * C::PPC) {
@@ -62,13 +62,13 @@ xform_small_kernel(const XformParams X) {
         u32 v[16];
         if constexpr (MODE == MODE_NTT_INV) {
             // natural spectrum -> position rev(k) (the DIT's bit-reversed input)
-            __syncthreads();  // the previous row is done with buf
+            mc_sync();  // the previous row is done with buf
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 const int k = t + G * s;
                 buf[swz_xf(brev_k<K>(k))] = valid ? mul_shoup(__ldcs(gx + k), 1u, X.red_wp, p) : 0u;
             }
-            __syncthreads();
+            mc_sync();
 #pragma unroll
             for (int s = 0; s < 16; ++s) v[s] = buf[swz_xf(slot_pos<SBL>(t, s))];
             inv_lower_chain1<K, Plan<K>::NP - 1, LayXf, 16>(buf, v, t, X.cs, W, LayXf());
@@ -86,14 +86,14 @@ xform_small_kernel(const XformParams X) {
             fwd_top<K, NT>(v, X.z, t, X.cs, W);
             fwd_lower_chain1<K, 0, LayXf, NT>(buf, v, t, X.cs, W, LayXf());
             // v[s] = X[rev(x)] at x = slot_pos<SBL>(t, s); stage it for a coalesced store
-            __syncthreads();
+            mc_sync();
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 const int x = slot_pos<SBL>(t, s);
                 if (NT >= 16 || (x >> (K - 4)) < NT)
                     buf[swz_xf(MODE == MODE_NTT_FWD ? brev_k<K>(x) : x)] = v[s];
             }
-            __syncthreads();
+            mc_sync();
             if (valid) {
 #pragma unroll
                 for (int s = 0; s < 16; ++s) {
