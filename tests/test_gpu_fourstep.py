@@ -119,6 +119,27 @@ def test_three_primes_fused_crt_path(orc, z1, z2):
     assert np.array_equal(got, want), (z1, z2)
 
 
+@pytest.mark.parametrize("z1,z2,off", [(1 << 20, 1 << 20, 0), (300007, 200003, 1),
+                                        (1 << 21, 5, 0), (77, 1 << 21, 3)])
+def test_three_primes_words_and_alignment(orc, z1, z2, off):
+    """Four-step sizes with full 32-bit input words (reduced mod each prime
+    on load), lopsided operands, and operands that are not 16-byte aligned
+    (off words into a buffer: no tensor-map loads) -- exact limbs vs the
+    oracle."""
+    rng = np.random.default_rng(z1 + 3 * z2 + off)
+    a = rng.integers(0, 1 << 32, z1, dtype=np.uint64).astype(np.uint32)
+    b = rng.integers(0, 1 << 32, z2, dtype=np.uint64).astype(np.uint32)
+    a[:3] = 0xFFFFFFFF
+    b[-3:] = 0xFFFFFFFF
+    abuf = torch.zeros(z1 + off, dtype=torch.int32, device="cuda")
+    bbuf = torch.zeros(z2 + off, dtype=torch.int32, device="cuda")
+    abuf[off:] = torch.from_numpy(a.view(np.int32)).cuda()
+    bbuf[off:] = torch.from_numpy(b.view(np.int32)).cuda()
+    got = to_u32_np(mc.mul_three_primes_tensor(abuf[off:], bbuf[off:]))
+    want = orc.mul_three_primes(a, b, threads=8)
+    assert np.array_equal(got, want), (z1, z2, off)
+
+
 @pytest.mark.parametrize("z1,z2", [(1, 1), (1, 9), (5, 3), (300, 200), (4096, 4096),
                                     (5000, 3), (20000, 17000)])
 def test_three_primes_small_exact(orc, z1, z2):
