@@ -162,11 +162,12 @@ row_conv_kernel(const FourParams P, int KR) {
             inv_lower_chain<KC, 16, Plan<KC>::NP - 1, AR>(bufA, va, t, P.cs, W);
             ItftTop<KC, 16, 16, 0, AR>::run(va, t, P.cs, W);
             if (valid) {
+                const int rot = out_rot(P, P.prod0 + prod);
 #pragma unroll
                 for (int s = 0; s < 16; ++s) {
                     const int x = t + G * s;
                     const uint2 w = __ldg(twi + x);  // w^-(x f1) * L^-1 * 2^32
-                    rowA[x] = mul_inv_t<AR>(va[s], w.x, w.y, p);
+                    rowA[(x + rot) & (Cn - 1)] = mul_inv_t<AR>(va[s], w.x, w.y, p);
                 }
             }
             mc_sync();
@@ -209,10 +210,12 @@ row_conv_kernel(const FourParams P, int KR) {
         inv_lower_chain<KC, 16, Plan<KC>::NP - 1, AR>(bufA, va, t, P.cs, W);
         ItftTop<KC, 16, 16, 0, AR>::run(va, t, P.cs, W);
         if (valid) {
+            const int rot = out_rot(P, P.prod0 + prod);
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 const uint2 bt = beta[16 + s];
-                rowA[t + G * s] = mul_inv_t<AR>(mul_inv_t<AR>(va[s], ai, aip, p), bt.x, bt.y, p);
+                rowA[(t + G * s + rot) & (Cn - 1)] =
+                    mul_inv_t<AR>(mul_inv_t<AR>(va[s], ai, aip, p), bt.x, bt.y, p);
             }
         }
         mc_sync();

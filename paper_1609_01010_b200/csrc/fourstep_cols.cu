@@ -61,12 +61,12 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_fwd
 // check (tile-uniform branch); the others store through one base pointer.
 template <int KR, int KC, int NT, int AR>
 __device__ __forceinline__ void store_col(u32 *dst, const u32 (&v)[16], int t, long long col,
-                                          long long tile_col0, const FourParams &P) {
+                                          long long tile_maxcol, const FourParams &P) {
     using C = ColCfg<KR>;
     constexpr long long Ccols = 1ll << KC;
     constexpr long long SLOT = (long long)C::G * Ccols;  // position stride of a slot
     u32 *base = dst + (long long)t * Ccols + col;
-    if (15 * SLOT + (long long)(C::G - 1) * Ccols + tile_col0 + C::TC - 1 < P.n) {
+    if (15 * SLOT + (long long)(C::G - 1) * Ccols + tile_maxcol < P.n) {
 #pragma unroll
         for (int s = 0; s < 16; ++s) __stcs(base + s * SLOT, canon_t<AR>(v[s], P.cs.p));
     } else {
@@ -100,7 +100,11 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_inv
     u32 *dst = P.c + prod * P.ldc;
     const int c = threadIdx.x % C::TC;
     const int t = threadIdx.x / C::TC;
-    const long long col = (long long)blockIdx.x * C::TC + c;
+    // scratch column j holds spectrum column (j - rot) mod C (out_rot)
+    const int rot = out_rot(P, prod);
+    const long long j0 = (long long)blockIdx.x * C::TC;
+    const long long col = (j0 + c - rot) & (Ccols - 1);
+    const long long maxcol = j0 >= rot ? j0 - rot + C::TC - 1 : Ccols - 1;
     mc_sync();
 
     u32 v[16];
@@ -108,12 +112,12 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_inv
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
         const int row = slot_pos<SB>(t, s);
-        v[s] = (NT >= 16 || (row >> (KR - 4)) < NT) ? src[(long long)row * Ccols + col] : 0u;
+        v[s] = (NT >= 16 || (row >> (KR - 4)) < NT) ? src[(long long)row * Ccols + j0 + c] : 0u;
     }
     LayCol<C::TC> lay{c};
     inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, NT, AR>(tile, v, t, P.cs, W, lay);
     inv_top<KR, NT, AR>(v, t, P.cs, W);
-    store_col<KR, KC, NT, AR>(dst, v, t, col, (long long)blockIdx.x * C::TC, P);
+    store_col<KR, KC, NT, AR>(dst, v, t, col, maxcol, P);
 }
 
 // Forward column pass, TMA variant: persistent CTAs walk the (product,
@@ -264,8 +268,10 @@ __global__ void __launch_bounds__(1024, 1) col_inv_async_kernel(const FourParams
         inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, NT, AR>(buf, v, t, P.cs, W, lay);
         inv_top<KR, NT, AR>(v, t, P.cs, W);
         u32 *dst = P.c + (P.prod0 + pc) * P.ldc;
-        const long long col = (long long)ct * C::TC + c;
-        store_col<KR, KC, NT, AR>(dst, v, t, col, (long long)ct * C::TC, P);
+        const int rot = out_rot(P, P.prod0 + pc);  // scratch column j = spectrum column j - rot
+        const long long j0 = (long long)ct * C::TC;
+        const long long col = (j0 + c - rot) & (Ccols - 1);
+        store_col<KR, KC, NT, AR>(dst, v, t, col, j0 >= rot ? j0 - rot + C::TC - 1 : Ccols - 1, P);
         k ^= 1;
     }
 }
