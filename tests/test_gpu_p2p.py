@@ -92,3 +92,36 @@ def test_crt3_slice_matches_full(orc):
                                         cnt, st))
     torch.cuda.synchronize()
     assert torch.equal(out, full)
+
+
+def _nccl_worker(rank, port, out_dir):
+    sys.path.insert(0, REPO)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=rank, world_size=1, device_id=torch.device("cuda:0"))
+    from paper_1609_01010_b200 import distributed as D
+
+    assert dist.get_backend() == "nccl"
+    a_np, b_np = _inputs(9000, 7001)
+    a = torch.from_numpy(a_np.view(np.int32)).cuda()
+    b = torch.from_numpy(b_np.view(np.int32)).cuda()
+    # the stream-ordered barrier is a one-word NCCL all-reduce queued behind
+    # the product kernels; the limbs copied after it must be complete
+    r = D.mul_three_primes_distributed(a, b, dst=0)
+    D._stream_barrier(None, a.device)
+    np.save(os.path.join(out_dir, "nccl_dist.npy"), r.cpu().numpy().view(np.uint32))
+    r = D.mul_three_primes_p2p(a, b, dst=0)
+    np.save(os.path.join(out_dir, "nccl_p2p.npy"), r.cpu().numpy().view(np.uint32))
+    dist.destroy_process_group()
+
+
+def test_nccl_process_group_world_size_1(tmp_path, orc):
+    """The NCCL backend on the box's one GPU: process group, stream-ordered
+    barrier (all-reduce) and both distributed three-primes entry points.
+    World sizes > 1 need one GPU per rank (NCCL rejects two ranks on one
+    device); their orchestration is covered by the gloo tests."""
+    mp.spawn(_nccl_worker, args=(_free_port(), str(tmp_path)), nprocs=1, join=True)
+    want = orc.mul_three_primes(*_inputs(9000, 7001))
+    for name in ("nccl_dist", "nccl_p2p"):
+        assert np.array_equal(np.load(tmp_path / f"{name}.npy"), want), name
