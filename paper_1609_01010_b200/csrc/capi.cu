@@ -138,9 +138,10 @@ struct StreamIn {
 // reference's tft x2 + pointwise + itft (convolve.py:230-253).
 static bool split_tft_on(int K, int n, long long batch) {
     static const bool off = [] { const char *e = getenv("MC_NO_SPLIT_TFT"); return e && *e; }();
-    if (off || K < 5 || K > kSmallMaxK + 1) return false;
+    if (off || K < 5 || K - 1 > kFourStepMaxK) return false;
     const int half = 1 << (K - 1), m = n - half;
-    if (m < 1 || m > (1 << K) / 8) return false;
+    // the tail is a fused launch: 2m - 1 <= 2^13
+    if (m < 1 || m > (1 << K) / 8 || 2 * m - 1 > (1 << kSmallMaxK)) return false;
     // two launches: only where the kernels, not the launch latency, dominate
     return K >= 10 || batch * (1ll << K) >= (1ll << 20);
 }
@@ -157,13 +158,19 @@ static mc_status split_tft(const u32 *a, long long lda, int z1, const u32 *b, lo
     const FieldTables *T1, *T2;
     mc_status s = get_tables(p, K - 1, &T1);
     if (s != MC_OK) return s;
-    ConvSmallParams H = make_params(T1, a, lda, z1, b, ldb, z2, c, ldc, half, batch);
-    H.fold = 1;
-    H.ar = lazy_ok(p) ? 1 : 2;
-    setup_tma(H, K - 1, allow_tma);
-    cudaError_t e = launch_small(K - 1, H, 16, st);
-    note_launches(1);
-    if (e != cudaSuccess) return cuda_fail(e, "split tft head launch");
+    cudaError_t e;
+    if (K - 1 <= kSmallMaxK) {
+        ConvSmallParams H = make_params(T1, a, lda, z1, b, ldb, z2, c, ldc, half, batch);
+        H.fold = 1;
+        H.ar = lazy_ok(p) ? 1 : 2;
+        setup_tma(H, K - 1, allow_tma);
+        e = launch_small(K - 1, H, 16, st);
+        note_launches(1);
+        if (e != cudaSuccess) return cuda_fail(e, "split tft head launch");
+    } else {  // four-step head: circular L/2-point product of the folded operands
+        s = fourstep_conv(0, a, lda, z1, b, ldb, z2, c, ldc, batch, p, st, K - 1, false, true);
+        if (s != MC_OK) return s;
+    }
     const int y1 = std::min(z1, m), y2 = std::min(z2, m);
     const int K2 = std::max(4, ceil_log2(y1 + y2 - 1));
     if ((s = get_tables(p, K2, &T2)) != MC_OK) return s;

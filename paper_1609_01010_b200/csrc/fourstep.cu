@@ -554,11 +554,18 @@ cudaError_t fourstep_inv_cols(FourPlan &F, cudaStream_t st) {
 
 mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u32 *b,
                         long long ldb, int z2, u32 *c, long long ldc, long long batch, u32 p,
-                        cudaStream_t st, int circ_log2L, bool reduce_inputs) {
+                        cudaStream_t st, int circ_log2L, bool reduce_inputs, bool fold) {
     FourPlan F;
     mc_status s = fourstep_plan(engine, a, lda, z1, b, ldb, z2, c, ldc, batch, p, circ_log2L,
                                 reduce_inputs, &F);
     if (s != MC_OK) return s;
+    if (fold) {  // split truncated product head: circular product of the folded operands
+        if (circ_log2L < 0 || F.K > kFourStepMaxK) return fail(MC_EINVAL, "fold needs a circular plan");
+        F.P.z1 = z1;
+        F.P.z2 = z2;
+        F.P.fold = 1;
+        F.tma.ok = 0;  // plain column loads (the tensor maps cover L words)
+    }
     if (F.K > kFourStepMaxK)  // L = 2^27 (p3 only): level-scheduled transforms
         return levels_conv(a, lda, z1, b, ldb, z2, c, ldc, batch, p, F.K,
                            circ_log2L >= 0 ? (1ll << circ_log2L) : (long long)z1 + z2 - 1, st);

@@ -33,6 +33,7 @@ mc_status levels_conv(const u32 *a, long long lda, int z1, const u32 *b, long lo
 
 mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u32 *b,
                         long long ldb, int z2, u32 *c, long long ldc, long long batch, u32 p,
-                        cudaStream_t st, int circ_log2L, bool reduce_inputs = false);
+                        cudaStream_t st, int circ_log2L, bool reduce_inputs = false,
+                        bool fold = false);
 
 }  // namespace mc

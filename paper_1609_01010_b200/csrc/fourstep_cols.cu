@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_fwd
     for (int s = 0; s < 16; ++s) {
         const long long idx = (long long)(t + C::G * s) * Ccols + col;
         u32 x = idx < z ? __ldcs(src + idx) : 0u;
+        const long long L = Ccols << KR;
+        if (P.fold && idx + L < z) x = add_mod(x, __ldcs(src + idx + L), p);
         if (P.reduce) x = mul_t<AR>(x, 1u, P.red_wp, p);
         v[s] = x;
     }

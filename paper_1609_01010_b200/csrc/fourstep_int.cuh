@@ -41,6 +41,7 @@ struct FourParams {
     // w_L^(x * rev(r)), twi[r][x] = w_L^-(x * rev(r)) * L^-1 * 2^32, Shoup pairs
     const uint2 *twf, *twi;
     int row_prefetch;  // L2 bulk prefetch of the next row (the row pass's data exceeds L2)
+    int fold;  // split truncated product head: operands longer than L fold x + L onto x
 };
 
 // Column rotation of the product spectrum.  The row pass writes spectrum

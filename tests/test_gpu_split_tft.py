@@ -38,18 +38,21 @@ def _check(orc, p, z1, z2, rows, seed, ld=None):
     a = orc.gen_u32(seed, 0, z1, rows, z1, p)
     b = orc.gen_u32(seed, 1, z2, rows, z2, p)
     want, _, _ = orc.conv_batch(a, b, p, orc.ENGINE_TFT)
-    before = _native.launch_count()
-    got = to_u32_np(mc.conv_batch(_dev(a, ld), _dev(b, ld), p, engine="tft"))
-    launches = _native.launch_count() - before
+    ad, bd = _dev(a, ld), _dev(b, ld)
+    got = to_u32_np(mc.conv_batch(ad, bd, p, engine="tft"))
     assert np.array_equal(got, want), (p, z1, z2, rows, np.argwhere(got != want)[:4].tolist())
-    return launches
+    before = _native.launch_count()  # tables are built now: count one call's kernels
+    mc.conv_batch(ad, bd, p, engine="tft")
+    return _native.launch_count() - before
 
 
-@pytest.mark.parametrize("K", list(range(5, 15)))
+@pytest.mark.parametrize("K", list(range(5, 17)))
 def test_split_boundaries(orc, K):
+    """K <= 14: fused head; K = 15, 16: four-step head (circular L/2-point
+    product of the folded operands, plain column loads)."""
     L = 1 << K
     for m in sorted({1, 2, 3, 7, L // 16 - 1, L // 16, L // 16 + 1, L // 8 - 1, L // 8}):
-        if m < 1 or m > L // 8:
+        if m < 1 or m > min(L // 8, 4096):
             continue
         n = L // 2 + m
         for z1 in sorted({1, 2, (n + 1) // 2, m, L // 2, L // 2 + 1}):
@@ -57,14 +60,15 @@ def test_split_boundaries(orc, K):
             if z1 < 1 or z2 < 1:
                 continue
             launches = _check(orc, P3, z1, z2, _rows(K), seed=K * 1000 + m)
-            assert launches == 2, (K, m, z1, launches)  # the head and the tail
+            # the head (one fused launch, or three four-step passes) and the tail
+            assert launches == (2 if K <= 14 else 4), (K, m, z1, launches)
 
 
 @pytest.mark.parametrize("p", [P1, P2, P3])
 def test_split_strided_and_aligned(orc, p):
-    for K in (11, 12, 13, 14):
+    for K in (11, 12, 13, 14, 15):
         L = 1 << K
-        for m in (5, L // 8):
+        for m in (5, min(L // 8, 4096)):
             n = L // 2 + m
             z1 = (n + 1) // 2
             z2 = n + 1 - z1
@@ -88,11 +92,16 @@ def test_split_all_p_minus_1(orc):
 
 
 def test_split_not_taken_past_eighth(orc):
-    """m > L/8 keeps the single relaxed-truncation launch."""
+    """m > L/8 keeps the single relaxed-truncation launch (fused sizes) or
+    the relaxed four-step passes."""
     L = 4096
     n = L // 2 + L // 8 + 1
     z1 = (n + 1) // 2
     assert _check(orc, P2, z1, n + 1 - z1, 3, seed=5) == 1
+    L = 1 << 17
+    n = L // 2 + 4097  # tail beyond a fused launch
+    z1 = (n + 1) // 2
+    assert _check(orc, P3, z1, n + 1 - z1, 2, seed=6) == 3
 
 
 def test_split_poly_mul_counters():
