@@ -9,7 +9,7 @@ for k, r in d.get("all_configs", {}).items():
     ip = r.get("int_pipe", {})
     print(k, f"ms {r.get('ms_per_step', 0):.4f}", f"value {r['value']:.4g}",
           f"hbm {r.get('roofline', {}).get('frac', 0):.3f}",
-          f"int_nom {ip.get('nominal_frac', 0):.3f}",
+          f"int_nom {ip.get('frac', 0):.3f} int_prac {ip.get('practical_frac', 0):.3f}",
           f"e2e {r.get('e2e', {}).get('value', 0):.4g}",
           f"cpu {r.get('cpu_baseline', {}).get('value', 0):.4g}",
           f"launches {r.get('gpu_launches')}", r.get("launch"))
