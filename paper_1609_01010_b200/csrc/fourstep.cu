@@ -112,8 +112,10 @@ row_conv_kernel(const FourParams P, int KR) {
         const bool valid = gr < rows;
         if constexpr (TT) {
 #if MC_ROW_PREFETCH
-            if (P.row_prefetch && threadIdx.x == 0) {  // next row: operand + twist rows into L2
-                const long long ng = base + (long long)gridDim.x * RC::PPC;
+            // next rows of every row group: operand + twist rows into L2 (thread g
+            // prefetches group g's next row)
+            if (P.row_prefetch && threadIdx.x < RC::PPC) {
+                const long long ng = base + (long long)gridDim.x * RC::PPC + threadIdx.x;
                 if (ng < rows) {
                     const long long np = ng % P.chunk, nr = ng / P.chunk;
                     if (!STG) {

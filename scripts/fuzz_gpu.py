@@ -28,6 +28,9 @@ def check_conv(rng, stats):
     fp = mc.FourierPrime.from_modulus(p)
     maxlog = min(fp.two_adicity, 17)
     n = rng.randint(1, 1 << maxlog)
+    if rng.random() < 0.25 and maxlog >= 6:  # just past a power of two: split truncated product
+        k = rng.randint(5, maxlog - 1)
+        n = (1 << k) + rng.randint(1, max(1, (1 << k) // 4))
     z1 = rng.randint(1, n)
     z2 = n + 1 - z1
     L = 1 << (n - 1).bit_length() if n > 1 else 1

@@ -225,3 +225,21 @@ def test_beyond_the_two_adicity_raises():
     with pytest.raises(mc.UnsupportedSizeError) as ei:
         mc.conv_batch(a, a, p)
     assert ei.value.required_two_adicity == 24
+
+
+@pytest.mark.parametrize("K", [14, 16])
+def test_row_prefetch_every_group(orc, K, monkeypatch):
+    """The row pass's L2 prefetch (forced on: MC_ROW_PREFETCH=1) with two row
+    groups per CTA at K = 14 (2^10-point rows) and one at K = 16: results
+    unchanged, bit-exact vs the oracle."""
+    monkeypatch.setenv("MC_ROW_PREFETCH", "1")
+    p = P2
+    n = (1 << K) - 3
+    z1 = (n + 1) // 2
+    a = orc.gen_u32(70 + K, 0, 0, 5, z1, p)
+    b = orc.gen_u32(70 + K, 1, 0, 5, n + 1 - z1, p)
+    want, _, _ = orc.conv_batch(a, b, p, threads=8)
+    at = torch.from_numpy(a.view(np.int32)).cuda()
+    bt = torch.from_numpy(b.view(np.int32)).cuda()
+    got = to_u32_np(mc.conv_batch(at, bt, p, engine="fft_pad"))
+    assert np.array_equal(got, want)
