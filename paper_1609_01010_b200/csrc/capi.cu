@@ -79,6 +79,8 @@ static ConvSmallParams make_params(const FieldTables *T, const u32 *a, long long
     P.tf = T->tf;
     P.ti = T->ti;
     memcpy(P.c16f, T->h16f, sizeof(P.c16f));
+    memcpy(P.c16fd, T->h16fd, sizeof(P.c16fd));
+    memcpy(P.c16id, T->h16id, sizeof(P.c16id));
     memcpy(P.c16i, T->h16i, sizeof(P.c16i));
     memcpy(P.mlev, T->mlev, sizeof(P.mlev));
     memcpy(P.hinv, T->hinv, sizeof(P.hinv));

@@ -65,6 +65,8 @@ struct ConvSmallParams {
     int za16, zb16;    // words of a / b rows covered by the bulk copies (multiple of 4)
     uint2 c16f[16];    // tf[1..15] / ti[1..15]: the thread-invariant twiddles of the
     uint2 c16i[16];    // lowest pass (h <= 8), read from the constant bank
+    double c16fd[16];  // RD(w / p) of the same twiddles (FP64-quotient products, MC_F64Q)
+    double c16id[16];
     int ar;            // arithmetic mode of the launch (modarith.cuh): 1 or 2
     int bulk_out;      // write product rows by bulk copies from shared memory (PPC == 1;
                        // zero-copy host output)
@@ -227,6 +229,18 @@ __device__ __forceinline__ void fwd_top(u32 (&v)[16], int z, int t, const ConvSm
 #endif
 
 // ---------------------------------------------------------------- lower passes
+// Levels h = 2^b of the lowest pass (SB = 0, constant twiddles) whose
+// products take the FP64-quotient form (modarith.cuh mul_f64q_lazy): bit b
+// of MC_F64Q.  Off: with h = 8 and 4 on FP64 (-DMC_F64Q=0xC) config 2 ran
+// 122.9 vs 121.1 us and config 3 4.03 vs 3.91 ms, config 4 1.058 vs 1.062 ms
+// (scripts/variant_ab.sh, two alternations on one box).  The fused kernel is
+// bound by issue and latency more than by the FMA-heavy pipe, so the extra
+// DADD / DFMA issue slots cost more than the freed IMAD.HI cycles; the
+// isolated pass, which has no exchanges, gains 7% (profiles/r02/ubench_r02.json).
+#ifndef MC_F64Q
+#define MC_F64Q 0
+#endif
+
 template <int K, int LO, int HI, int SB, int AR = 0, class TW = Tw>
 __device__ __forceinline__ void fwd_lower(u32 (&v)[16], int t, const ConvSmallParams &P,
                                           const TW &W) {
@@ -243,6 +257,8 @@ __device__ __forceinline__ void fwd_lower(u32 (&v)[16], int t, const ConvSmallPa
                 const int j = s & (h - 1);
                 if (j == 0) {  // w = 1: no multiplication
                     bfly_dif1_t<AR>(v[s], v[s | (1 << sbit)], p);
+                } else if ((MC_F64Q >> b) & 1) {
+                    bfly_dif_q_t<AR>(v[s], v[s | (1 << sbit)], P.c16f[h + j].x, P.c16fd[h + j], p);
                 } else {
                     const uint2 w = P.c16f[h + j];
                     bfly_dif_t<AR>(v[s], v[s | (1 << sbit)], w.x, w.y, p);
@@ -272,6 +288,8 @@ __device__ __forceinline__ void inv_lower(u32 (&v)[16], int t, const ConvSmallPa
                 const int j = s & (h - 1);
                 if (j == 0) {  // w = 1
                     bfly_dit1_t<AR>(v[s], v[s | (1 << sbit)], p);
+                } else if ((MC_F64Q >> b) & 1) {
+                    bfly_dit_q_t<AR>(v[s], v[s | (1 << sbit)], P.c16i[h + j].x, P.c16id[h + j], p);
                 } else {
                     const uint2 w = P.c16i[h + j];
                     bfly_dit_t<AR>(v[s], v[s | (1 << sbit)], w.x, w.y, p);

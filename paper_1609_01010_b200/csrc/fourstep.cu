@@ -496,6 +496,8 @@ mc_status fourstep_plan(int engine, const u32 *a, long long lda, int z1, const u
     // tf[h + j] = w_{2h}^j does not depend on L: the lowest-pass constants of
     // the column and row transforms are the same
     memcpy(P.cs.c16f, TR->h16f, sizeof(P.cs.c16f));
+    memcpy(P.cs.c16fd, TR->h16fd, sizeof(P.cs.c16fd));
+    memcpy(P.cs.c16id, TR->h16id, sizeof(P.cs.c16id));
     memcpy(P.cs.c16i, TR->h16i, sizeof(P.cs.c16i));
     P.cs.pinv = TL->pinv;
     P.cs.linv_mont = TL->linv_mont;  // 1/L for the whole transform

@@ -203,6 +203,58 @@ __device__ __forceinline__ void bfly_dit_neg_t(u32 &a, u32 &b, u32 w, u32 wp, u3
     }
 }
 
+// ---------------------------------------------------------------- FP64 quotient
+// Shoup's product with the quotient estimated on the FP64 pipe instead of
+// IMAD.HI: x is made exact in a double by one DADD (2^52 bias), one DFMA.RZ
+// forms floor(x * wd) + 2^52 with wd = RD(w / p) <= w / p, so q is floor(x w / p)
+// or one less and r = x*w - q*p lies in [0, 2p) exactly as with Shoup.  The
+// FMA-heavy pipe, which the Shoup products keep busiest (IMAD.HI holds it two
+// cycles), then carries two IMADs instead of four slots; the otherwise idle
+// FP64 pipe takes the rest.  Measured on the isolated radix-16 pass
+// (scripts/ubench.py): a quarter of the butterflies this way, 10.95 -> 11.73
+// butterflies/clk/SM; all of them, 10.8 (the issue slots then bind).
+__device__ __forceinline__ u32 mul_f64q_lazy(u32 x, u32 w, double wd, u32 p) {
+    const double xd = __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
+    const double qd = __fma_rz(xd, wd, 4503599627370496.0);
+    return x * w - (u32)__double2loint(qd) * p;
+}
+
+template <int AR>
+__device__ __forceinline__ void bfly_dif_q_t(u32 &a, u32 &b, u32 w, double wd, u32 p) {
+    if constexpr (MC_AR(AR) == 1) {
+        const u32 s = a + b;
+        b = mul_f64q_lazy(a - b + 2 * p, w, wd, p);
+        a = min(s, s - 2 * p);
+    } else {
+        const u32 s = a + b;
+        const u32 r = mul_f64q_lazy(a - b + p, w, wd, p);
+        a = min(s, s - p);
+        b = min(r, r - p);
+    }
+}
+
+template <int AR>
+__device__ __forceinline__ void bfly_dit_q_t(u32 &a, u32 &b, u32 w, double wd, u32 p) {
+    if constexpr (MC_AR(AR) == 1) {
+        const u32 x = min(a, a - 2 * p);
+        const u32 t = mul_f64q_lazy(b, w, wd, p);
+        a = x + t;
+        b = x - t + 2 * p;
+    } else if constexpr (MC_AR(AR) == 2) {
+        const u32 x = min(a, a - p);
+        const u32 r = mul_f64q_lazy(b, w, wd, p);
+        const u32 t = min(r, r - p);
+        a = x + t;
+        b = x - t + p;
+    } else {
+        const u32 r = mul_f64q_lazy(b, w, wd, p);
+        const u32 t = min(r, r - p);
+        const u32 s = a + t, d = a - t + p;
+        a = min(s, s - p);
+        b = min(d, d - p);
+    }
+}
+
 // DIT butterfly with w = 1
 template <int AR>
 __device__ __forceinline__ void bfly_dit1_t(u32 &a, u32 &b, u32 p) {

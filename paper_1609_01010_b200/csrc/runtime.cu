@@ -1,4 +1,5 @@
 // Host runtime: field arithmetic, twiddle-table cache, error state.
+#include <cmath>
 #include <cstdlib>
 #include <atomic>
 #include <cstring>
@@ -250,6 +251,9 @@ mc_status get_tables(u32 p, int log2L, const FieldTables **out) {
     for (u64 i = 0; i < 16 && i < hf.size(); ++i) {
         T->h16f[i] = hf[i];
         T->h16i[i] = hi[i];
+        // RD(w / p): the round-to-nearest quotient stepped down one ulp is <= w / p
+        T->h16fd[i] = std::nextafter((double)hf[i].x / (double)p, 0.0);
+        T->h16id[i] = std::nextafter((double)hi[i].x / (double)p, 0.0);
     }
     // merged table: L - 1 + log2 L entries, padded to a multiple of 2 (uint4 copies)
     std::vector<uint2> hm;

@@ -59,6 +59,8 @@ struct FieldTables {
     int tm_entries = 0;
     uint2 h16f[16] = {};  // host copies of tf[0..15] / ti[0..15]
     uint2 h16i[16] = {};
+    double h16fd[16] = {};  // RD(w / p) of the same twiddles (FP64-quotient products)
+    double h16id[16] = {};
     Shoup mlev[5] = {};   // fused-kernel top-level constants (see ConvSmallParams)
     Shoup hinv[5] = {};
 };

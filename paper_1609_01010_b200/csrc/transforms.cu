@@ -581,6 +581,8 @@ static mc_status xform_small(int mode, const u32 *x, long long ldx, int z, u32 *
     X.cs.tf = T->tf;
     X.cs.ti = T->ti;
     memcpy(X.cs.c16f, T->h16f, sizeof(X.cs.c16f));
+    memcpy(X.cs.c16fd, T->h16fd, sizeof(X.cs.c16fd));
+    memcpy(X.cs.c16id, T->h16id, sizeof(X.cs.c16id));
     memcpy(X.cs.c16i, T->h16i, sizeof(X.cs.c16i));
     memcpy(X.cs.mlev, T->mlev, sizeof(X.cs.mlev));
     memcpy(X.cs.hinv, T->hinv, sizeof(X.cs.hinv));

@@ -10,17 +10,7 @@
 
 namespace mc {
 
-// Shoup-style lazy product with the quotient estimated on the FP64 pipe
-// instead of IMAD.HI: q = floor(x * wd) with wd = RD(w / p) (one DADD makes x
-// exact in a double, one DFMA.RZ adds 2^52 so the integer quotient lands in
-// the low mantissa word), r = x*w - q*p in [0, 2p) as with Shoup.  Probe of
-// whether the FP64 pipe can take the high-product half of the work.
-__device__ __forceinline__ u32 mul_f64q_lazy(u32 x, u32 w, double wd, u32 p) {
-    const double xd = __hiloint2double(0x43300000, (int)x) - 4503599627370496.0;
-    const double qd = __fma_rz(xd, wd, 4503599627370496.0);
-    const u32 q = (u32)__double2loint(qd);
-    return x * w - q * p;
-}
+// mul_f64q_lazy (modarith.cuh): the FP64-quotient Shoup product.
 
 template <int KIND>
 __global__ void __launch_bounds__(256) ubench_kernel(u32 *out, u32 seed, int iters, u32 p,
@@ -94,7 +84,10 @@ __device__ __forceinline__ void bfly_variant(u32 &a, u32 &b, u32 w, u32 wp, u32 
 // A radix-16 DIF register pass on two operands (32 butterflies each, one
 // LDS.64 twiddle per butterfly) repeated `iters` times with no exchange and
 // no barrier: the butterfly stream of conv_small_kernel in isolation.
-template <int MINB, int MODE>
+// MIX > 0: the MIX lowest levels of each pass take the FP64-quotient
+// product (MODE 4), the others MODE: can the FP64 pipe relieve the
+// FMA-heavy one for a share of the butterflies?
+template <int MINB, int MODE, int MIX = 0>
 __global__ void __launch_bounds__(256, MINB) pass_bench_kernel(const uint2 *tw_g, u32 *out,
                                                                 int iters, u32 p) {
     __shared__ uint2 tw[4096];
@@ -115,8 +108,13 @@ __global__ void __launch_bounds__(256, MINB) pass_bench_kernel(const uint2 *tw_g
             for (int s = 0; s < 16; ++s) {
                 if (s & H) continue;
                 const uint2 w = tw[(H * 256 + t + 16 * (s & (2 * H - 1))) & 4095];
-                bfly_variant<MODE>(va[s], va[s + H], w.x, w.y, p);
-                bfly_variant<MODE>(vb[s], vb[s + H], w.x, w.y, p);
+                if (lv < MIX) {
+                    bfly_variant<4>(va[s], va[s + H], w.x, w.y, p);
+                    bfly_variant<4>(vb[s], vb[s + H], w.x, w.y, p);
+                } else {
+                    bfly_variant<MODE>(va[s], va[s + H], w.x, w.y, p);
+                    bfly_variant<MODE>(vb[s], vb[s + H], w.x, w.y, p);
+                }
             }
         }
     }
@@ -132,7 +130,8 @@ extern "C" {
 
 // Butterflies per clock per SM of the isolated register pass:
 // rates[0] MODE 0 at 2 CTAs/SM, rates[1] MODE 0 at 4 CTAs/SM,
-// rates[2..5] MODES 1..4 at 2 CTAs/SM (see bfly_variant).
+// rates[2..5] MODES 1..4 at 2 CTAs/SM (see bfly_variant), rates[6..8] MODE 0
+// with the 1, 2 or 3 lowest levels of each pass on the FP64-quotient product.
 mc_status mc_ubench_pass(double *rates) {
     using namespace mc;
     const int sms = sm_count();
@@ -155,7 +154,7 @@ mc_status mc_ubench_pass(double *rates) {
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     const int iters = 200;
-    for (int k = 0; k < 6; ++k) {
+    for (int k = 0; k < 9; ++k) {
         const int per_sm = k == 1 ? 4 : 2;
         const int blocks = sms * per_sm;
         for (int rep = 0; rep < 2; ++rep) {
@@ -167,6 +166,9 @@ mc_status mc_ubench_pass(double *rates) {
                 case 3: pass_bench_kernel<2, 2><<<blocks, 256>>>(tw, out, iters, p); break;
                 case 4: pass_bench_kernel<2, 3><<<blocks, 256>>>(tw, out, iters, p); break;
                 case 5: pass_bench_kernel<2, 4><<<blocks, 256>>>(tw, out, iters, p); break;
+                case 6: pass_bench_kernel<2, 0, 1><<<blocks, 256>>>(tw, out, iters, p); break;
+                case 7: pass_bench_kernel<2, 0, 2><<<blocks, 256>>>(tw, out, iters, p); break;
+                case 8: pass_bench_kernel<2, 0, 3><<<blocks, 256>>>(tw, out, iters, p); break;
             }
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
