@@ -71,15 +71,42 @@ def _dist():
     return ws, rank, local
 
 
+def tft_schedule(cfg) -> str:
+    """How the library runs a config's product (capi.cu conv_dispatch /
+    split_tft_on / tft_full_from, restated): the truncated engine's
+    schedule depends on how far n lies past L/2."""
+    if cfg["engine"] == "three_primes":
+        return "three primes: four-step per prime on forked streams + fused inverse/CRT pass"
+    n = cfg["z1"] + cfg["z2"] - 1
+    K = (n - 1).bit_length()
+    L, G = 1 << K, 1 << max(0, K - 4)
+    if cfg["engine"] != "tft" or K <= 3:
+        return "complete transforms (fused)" if K <= 13 else "complete transforms (four-step)"
+    m = n - L // 2
+    lim = L // (16 if K <= 10 else 8)
+    if (5 <= K <= 27 and 1 <= m <= lim and 2 * m - 1 <= 8192
+            and (K >= 10 or cfg["batch"] * L >= (1 << 20))):
+        return f"split truncated product: L/2-point head + low-product tail (m = {m})"
+    nt = -(-n // G)
+    if K <= 13:
+        if nt >= (13 if K == 13 else 11):
+            return (f"complete transform: {nt} of 16 blocks rounded up to 16 (the truncated "
+                    "kernel is slower there, DESIGN.md section 3)")
+        return f"relaxed truncation: {nt} of 16 blocks (fused)"
+    return f"relaxed truncation: {nt} of 16 column blocks (four-step)"
+
+
 def lazy_share(cfg) -> float:
     """Share of the butterflies that run in the lazy-range arithmetic (AR=1,
-    p < 2^30 on complete transforms; modarith.cuh): its register pass has a
-    higher measured ceiling than the canonical one."""
+    p < 2^30; modarith.cuh): its register pass has a higher measured ceiling
+    than the canonical one.  The fused kernels use it for truncated and
+    complete transforms, the four-step passes for complete ones."""
     if cfg["engine"] == "three_primes":
         return 2.0 / 3.0  # p1, p2 lazy; p3 (31-bit) canonical forward
     n = cfg["z1"] + cfg["z2"] - 1
     L = 1 << (n - 1).bit_length()
-    complete = cfg["engine"] == "fft_pad" or -(-n // (L // 16)) == 16
+    complete = (cfg["engine"] == "fft_pad" or L <= 8192
+                or "truncation" not in tft_schedule(cfg))
     return 1.0 if (cfg["p"] < (1 << 30) and complete) else 0.0
 
 
@@ -588,6 +615,7 @@ def measure(cfg, args, ws: int, rank: int) -> dict:
         "e2e": e2e,
         "gpu_launches": int(launches_all),
         "launch": "cuda graph replay" if launches_per_step is not None else "eager",
+        "schedule": tft_schedule(cfg),
         "clocks": clk,
     }
     try:  # DRAM bytes and pipe utilisation per launch from a committed ncu capture

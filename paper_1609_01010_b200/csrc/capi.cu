@@ -142,8 +142,9 @@ static bool split_tft_on(int K, int n, long long batch) {
     static const bool off = [] { const char *e = getenv("MC_NO_SPLIT_TFT"); return e && *e; }();
     if (off || K < 5 || K - 1 > kFourStepMaxK) return false;
     const int half = 1 << (K - 1), m = n - half;
-    // the tail is a fused launch: 2m - 1 <= 2^13
-    if (m < 1 || m > (1 << K) / 8 || 2 * m - 1 > (1 << kSmallMaxK)) return false;
+    // the tail is a fused launch: 2m - 1 <= 2^13; up to K = 10 the split pays
+    // only for m <= L/16 (octave sweeps, profiles/r02/octave_*.csv)
+    if (m < 1 || m > (1 << K) / (K <= 10 ? 16 : 8) || 2 * m - 1 > (1 << kSmallMaxK)) return false;
     // two launches: only where the kernels, not the launch latency, dominate
     return K >= 10 || batch * (1ll << K) >= (1ll << 20);
 }
@@ -185,6 +186,22 @@ static mc_status split_tft(const u32 *a, long long lda, int z1, const u32 *b, lo
     note_launches(1);
     if (e != cudaSuccess) return cuda_fail(e, "split tft tail launch");
     return MC_OK;
+}
+
+// Relaxed truncation limit of the fused kernel.  It truncates at whole 16ths
+// (G-blocks); its lower passes skip only warps whose G-blocks are all
+// inactive (two blocks per warp at K = 12), and the truncated inverse's
+// van der Hoeven steps cost three products per cross butterfly.  Measured
+// over whole octaves (profiles/r02/octave_*.csv, p2 and p3): with 11..15 of
+// 16 blocks the truncated kernel ran 5-13% slower than the complete
+// transform at K <= 12, and at K = 13 with 13..15 blocks, so the tft engine
+// rounds NT up to 16 there (the relaxation's limit case: the product is the
+// same); NT <= 10 takes the split product.  MC_TFT_KEEP_NT=1 keeps the
+// truncated schedule (A/B, tests).
+static int tft_full_from(int K) {
+    const char *e = getenv("MC_TFT_KEEP_NT");
+    if (e && *e && *e != '0') return 17;
+    return K == 13 ? 13 : 11;
 }
 
 // engine 0 = fft_pad, 1 = tft; wrap != 0 => circular convolution of length L
@@ -235,13 +252,11 @@ static mc_status conv_dispatch(int engine, const u32 *a, long long lda, int z1, 
         if (engine == 1 && !circ) {
             const int G = 1 << (K - 4);
             nt = (n + G - 1) / G;
-            // relaxation: NT = 15 saves 1/16 of the work, less than the lazy
-            // (Harvey) arithmetic of the complete transform gains for p < 2^30
-            if (nt == 15 && lazy_ok(p)) nt = 16;
+            if (nt >= tft_full_from(K)) nt = 16;
         }
         if (batch > 0x7fffffffll * SmallCfg<4>::PPC)
             return fail(MC_EINVAL, "batch too large for one launch");
-        P.ar = (nt == 16 && lazy_ok(p)) ? 1 : 2;
+        P.ar = lazy_ok(p) ? 1 : 2;
         {  // bulk-copy epilogue: host output (zero copy), or forced for A/B runs
             static const bool force = [] { const char *e = getenv("MC_BULK_OUT"); return e && *e; }();
             P.bulk_out = ((host_out || force) && (1 << K) / 16 >= 128) ? 1 : 0;

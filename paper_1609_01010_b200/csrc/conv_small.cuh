@@ -595,7 +595,6 @@ constexpr int FL_WRAP = 8;    // split truncated product, tail: unwrap the head'
 template <int K, int NT, int AR = 0, int FL = 0>
 __global__ void __launch_bounds__(SmallCfg<K>::THREADS, SmallCfg<K>::MINB)
 conv_small_kernel(const ConvSmallParams P) {
-    static_assert(AR != 1 || NT == 16, "Harvey ranges only for complete transforms");
     using C = SmallCfg<K>;
     constexpr int L = C::L, T = C::T;
     extern __shared__ uint4 smem_raw[];

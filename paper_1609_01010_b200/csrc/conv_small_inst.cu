@@ -72,15 +72,18 @@ static cudaError_t launch_nt(const ConvSmallParams &P, cudaStream_t st) {
 #define MC_CAT(a, b) MC_CAT2(a, b)
 
 cudaError_t MC_CAT(launch_conv_small_k, MC_K)(const ConvSmallParams &P, int nt, cudaStream_t st) {
+    // truncated transforms take the Harvey ranges too when p < 2^30 (P.ar = 1):
+    // their pre-adds, cross butterflies and combines canonicalise their operands
+    const bool lz = P.ar == 1;
     switch (nt) {
-        case 9: return launch_nt<9, 2>(P, st);
-        case 10: return launch_nt<10, 2>(P, st);
-        case 11: return launch_nt<11, 2>(P, st);
-        case 12: return launch_nt<12, 2>(P, st);
-        case 13: return launch_nt<13, 2>(P, st);
-        case 14: return launch_nt<14, 2>(P, st);
-        case 15: return launch_nt<15, 2>(P, st);
-        case 16: return P.ar == 1 ? launch_nt<16, 1>(P, st) : launch_nt<16, 2>(P, st);
+        case 9: return lz ? launch_nt<9, 1>(P, st) : launch_nt<9, 2>(P, st);
+        case 10: return lz ? launch_nt<10, 1>(P, st) : launch_nt<10, 2>(P, st);
+        case 11: return lz ? launch_nt<11, 1>(P, st) : launch_nt<11, 2>(P, st);
+        case 12: return lz ? launch_nt<12, 1>(P, st) : launch_nt<12, 2>(P, st);
+        case 13: return lz ? launch_nt<13, 1>(P, st) : launch_nt<13, 2>(P, st);
+        case 14: return lz ? launch_nt<14, 1>(P, st) : launch_nt<14, 2>(P, st);
+        case 15: return lz ? launch_nt<15, 1>(P, st) : launch_nt<15, 2>(P, st);
+        case 16: return lz ? launch_nt<16, 1>(P, st) : launch_nt<16, 2>(P, st);
         default: return cudaErrorInvalidValue;
     }
 }

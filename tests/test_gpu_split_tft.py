@@ -60,8 +60,10 @@ def test_split_boundaries(orc, K):
             if z1 < 1 or z2 < 1:
                 continue
             launches = _check(orc, P3, z1, z2, _rows(K), seed=K * 1000 + m)
-            # the head (one fused launch, or three four-step passes) and the tail
-            assert launches == (2 if K <= 14 else 4), (K, m, z1, launches)
+            # the head (one fused launch, or three four-step passes) and the
+            # tail; up to K = 10 the split is taken for m <= L/16 only
+            want = (2 if K <= 14 else 4) if (K > 10 or m <= L // 16) else 1
+            assert launches == want, (K, m, z1, launches)
 
 
 @pytest.mark.parametrize("p", [P1, P2, P3])
@@ -116,3 +118,20 @@ def test_split_poly_mul_counters():
     r2 = mc.poly_mul(a, b, mc.ConvRequest(fp, engine="fft_pad"))
     assert r == r2 and len(r.coeffs) == 2060
     assert cnt.butterflies > 0
+
+
+@pytest.mark.parametrize("keep", ["0", "1"])
+@pytest.mark.parametrize("K", [7, 10, 12, 13])
+def test_truncated_schedule_both_ways(orc, K, keep, monkeypatch):
+    """NT = 11..15 of 16 blocks: the tft engine runs the complete transform
+    (measured faster), or with MC_TFT_KEEP_NT=1 the relaxed truncated
+    kernel (van der Hoeven inverse over the top four levels, Harvey ranges
+    for p < 2^30) -- both bit-exact vs the oracle's conv_tft."""
+    monkeypatch.setenv("MC_TFT_KEEP_NT", keep)
+    L = 1 << K
+    G = L // 16
+    for p in (P2, P3):
+        for nt in range(11, 16):
+            n = nt * G - (G // 3 if nt % 2 else 0)
+            for z1 in sorted({1, (n + 1) // 2, n - 3}):
+                _check(orc, p, z1, n + 1 - z1, 3, seed=K * 100 + nt)
