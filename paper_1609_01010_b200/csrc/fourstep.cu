@@ -525,7 +525,10 @@ mc_status fourstep_plan(int engine, const u32 *a, long long lda, int z1, const u
     if (engine == 1 && !circ) NT = (int)((n + (L >> 4) - 1) / (L >> 4));
     if (NT == 15 && lazy_ok(p)) NT = 16;  // as the fused path (capi.cu conv_dispatch)
     P.nrows = (long long)NT << (KR - 4);
-    P.cs.ar = (NT == 16 && lazy_ok(p)) ? 1 : 2;
+    // Harvey ranges for p < 2^30 on every pass: the row transforms are complete
+    // whatever NT, and the truncated column passes canonicalise the operands of
+    // their van der Hoeven steps like the fused kernel's
+    P.cs.ar = lazy_ok(p) ? 1 : 2;
     F->KC = KC;
     F->KR = KR;
     F->NT = NT;

@@ -353,13 +353,20 @@ template <int KR, int KC>
 static cudaError_t launch_nt(const FourParams &P, int NT, bool fwd, cudaStream_t st,
                              const ColTma *tma) {
     switch (NT) {
-        case 9: return launch_one<KR, KC, 9, 2>(P, fwd, st, tma);
-        case 10: return launch_one<KR, KC, 10, 2>(P, fwd, st, tma);
-        case 11: return launch_one<KR, KC, 11, 2>(P, fwd, st, tma);
-        case 12: return launch_one<KR, KC, 12, 2>(P, fwd, st, tma);
-        case 13: return launch_one<KR, KC, 13, 2>(P, fwd, st, tma);
-        case 14: return launch_one<KR, KC, 14, 2>(P, fwd, st, tma);
-        case 15: return launch_one<KR, KC, 15, 2>(P, fwd, st, tma);
+        case 9: return P.cs.ar == 1 ? launch_one<KR, KC, 9, 1>(P, fwd, st, tma)
+                                 : launch_one<KR, KC, 9, 2>(P, fwd, st, tma);
+        case 10: return P.cs.ar == 1 ? launch_one<KR, KC, 10, 1>(P, fwd, st, tma)
+                                 : launch_one<KR, KC, 10, 2>(P, fwd, st, tma);
+        case 11: return P.cs.ar == 1 ? launch_one<KR, KC, 11, 1>(P, fwd, st, tma)
+                                 : launch_one<KR, KC, 11, 2>(P, fwd, st, tma);
+        case 12: return P.cs.ar == 1 ? launch_one<KR, KC, 12, 1>(P, fwd, st, tma)
+                                 : launch_one<KR, KC, 12, 2>(P, fwd, st, tma);
+        case 13: return P.cs.ar == 1 ? launch_one<KR, KC, 13, 1>(P, fwd, st, tma)
+                                 : launch_one<KR, KC, 13, 2>(P, fwd, st, tma);
+        case 14: return P.cs.ar == 1 ? launch_one<KR, KC, 14, 1>(P, fwd, st, tma)
+                                 : launch_one<KR, KC, 14, 2>(P, fwd, st, tma);
+        case 15: return P.cs.ar == 1 ? launch_one<KR, KC, 15, 1>(P, fwd, st, tma)
+                                 : launch_one<KR, KC, 15, 2>(P, fwd, st, tma);
         case 16:
             return P.cs.ar == 1 ? launch_one<KR, KC, 16, 1>(P, fwd, st, tma)
                                 : launch_one<KR, KC, 16, 2>(P, fwd, st, tma);
