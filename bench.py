@@ -84,8 +84,10 @@ def tft_schedule(cfg) -> str:
         return "complete transforms (fused)" if K <= 13 else "complete transforms (four-step)"
     m = n - L // 2
     lim = L // (16 if K <= 10 else 8)
-    if (5 <= K <= 27 and 1 <= m <= lim and 2 * m - 1 <= 8192
-            and (K >= 10 or cfg["batch"] * L >= (1 << 20))):
+    big = K >= 10 or cfg["batch"] * L >= (1 << 20)
+    if K in (13, 14) and L // 8 < m <= L // 4:
+        return f"split truncated product: L/2-point head + twisted L/4-point piece (m = {m})"
+    if 5 <= K <= 27 and 1 <= m <= lim and 2 * m - 1 <= 8192 and big:
         return f"split truncated product: L/2-point head + low-product tail (m = {m})"
     nt = -(-n // G)
     if K <= 13:

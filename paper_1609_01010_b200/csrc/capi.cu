@@ -138,13 +138,28 @@ struct StreamIn {
 //         then c[x] = low[x], c[L/2 + x] = c0[x] - low[x] for x < m.
 // Work ~ L/2 + 2m points instead of L; exact, so bit-identical to the
 // reference's tft x2 + pointwise + itft (convolve.py:230-253).
+// Twisted quarter tail (m in (L/8, L/4]): the L/4-point product mod
+// (x^(L/4) - i) instead of a 2m-point low product.  Measured over whole
+// octaves (profiles/r02/octave_*.csv): +6% at K = 13 and +31% at K = 14 (whose
+// complete transform is four-step) over the complete transform, but -8..-10%
+// at K = 12 (the extra folds, twists and global twiddle loads outweigh a
+// quarter of a fast K = 12 product) and even with the relaxed four-step
+// truncation at K = 15; so K = 13, 14 only.
+static bool split_twist(int K, int m) {
+    static const bool off = [] { const char *e = getenv("MC_NO_SPLIT_TWIST"); return e && *e; }();
+    return !off && (K == 13 || K == 14) && m > (1 << K) / 8 && m <= (1 << K) / 4;
+}
+
 static bool split_tft_on(int K, int n, long long batch) {
     static const bool off = [] { const char *e = getenv("MC_NO_SPLIT_TFT"); return e && *e; }();
     if (off || K < 5 || K - 1 > kFourStepMaxK) return false;
     const int half = 1 << (K - 1), m = n - half;
-    // the tail is a fused launch: 2m - 1 <= 2^13; up to K = 10 the split pays
-    // only for m <= L/16 (octave sweeps, profiles/r02/octave_*.csv)
-    if (m < 1 || m > (1 << K) / (K <= 10 ? 16 : 8) || 2 * m - 1 > (1 << kSmallMaxK)) return false;
+    if (m < 1) return false;
+    if (!split_twist(K, m)) {
+        // low-product tail, a fused launch: 2m - 1 <= 2^13; up to K = 10 the
+        // split pays only for m <= L/16 (octave sweeps, profiles/r02/octave_*.csv)
+        if (m > (1 << K) / (K <= 10 ? 16 : 8) || 2 * m - 1 > (1 << kSmallMaxK)) return false;
+    }
     // two launches: only where the kernels, not the launch latency, dominate
     return K >= 10 || batch * (1ll << K) >= (1ll << 20);
 }
@@ -173,6 +188,29 @@ static mc_status split_tft(const u32 *a, long long lda, int z1, const u32 *b, lo
     } else {  // four-step head: circular L/2-point product of the folded operands
         s = fourstep_conv(0, a, lda, z1, b, ldb, z2, c, ldc, batch, p, st, K - 1, false, true);
         if (s != MC_OK) return s;
+    }
+    if (split_twist(K, m)) {
+        // c mod (x^(L/4) - i), i = w_L^(L/4): an L/4-point cyclic product of
+        // the operands folded by quarters and twisted by w_L^x; then
+        // c = c0 + (x^(L/2) - 1) h, h = (c0 mod (x^(L/4) - i) - c1) / 2
+        const int K2 = K - 2, Lq = 1 << K2;
+        const FieldTables *TK;
+        if ((s = get_tables(p, K, &TK)) != MC_OK) return s;
+        if ((s = get_tables(p, K2, &T2)) != MC_OK) return s;
+        ConvSmallParams Q = make_params(T2, a, lda, Lq, b, ldb, Lq, c, ldc, Lq, batch);
+        Q.tz1 = z1;
+        Q.tz2 = z2;
+        Q.twq_f = TK->tf + (1 << (K - 1));
+        Q.twq_i = TK->ti + (1 << (K - 1));
+        Q.qi = shoup((u32)powmod(TK->root, (u64)Lq, p), p);
+        Q.qhalf = shoup((u32)((p + 1) / 2), p);
+        Q.wrap_m = m;
+        Q.wrap_off = half;
+        Q.ar = lazy_ok(p) ? 1 : 2;
+        e = launch_small(K2, Q, 16, st);
+        note_launches(1);
+        if (e != cudaSuccess) return cuda_fail(e, "split tft twisted tail launch");
+        return MC_OK;
     }
     const int y1 = std::min(z1, m), y2 = std::min(z2, m);
     const int K2 = std::max(4, ceil_log2(y1 + y2 - 1));

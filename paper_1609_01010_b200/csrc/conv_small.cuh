@@ -78,8 +78,14 @@ struct ConvSmallParams {
     // operands folded on load, the tail launch (wrap_m = m) forms the low
     // product and unwraps: c[x] = low[x], c[wrap_off + x] = c0[x] - low[x].
     int fold;      // FL_FOLD launch: rows longer than L fold x + L onto x
-    int wrap_m;    // FL_WRAP launch: coefficients to unwrap (== n)
-    int wrap_off;  // FL_WRAP launch: half length of the full product transform
+    int wrap_m;    // FL_WRAP / FL_TWIST launch: coefficients to unwrap (n - L'/2)
+    int wrap_off;  // FL_WRAP / FL_TWIST launch: half length L'/2 of the full product transform
+    // FL_TWIST launch (quarter piece, L = L'/4 of the full transform L'): the
+    // operands' true lengths, w_L'^x / w_L'^-x (the full transform's top-stage
+    // tables, entries L'/2 + x), i = w_L'^(L'/4) and 1/2
+    int tz1, tz2;
+    const uint2 *twq_f, *twq_i;
+    Shoup qi, qhalf;
 };
 
 // Shared-memory swizzle of the exchanges: XOR of position bits [2,5) with
@@ -589,6 +595,7 @@ constexpr int FL_HOST = 1;    // bulk-store epilogue / streamed-input ready flag
 constexpr int FL_REDUCE = 2;  // operands are arbitrary words: reduce mod p on load
 constexpr int FL_FOLD = 4;    // split truncated product, head: fold rows longer than L
 constexpr int FL_WRAP = 8;    // split truncated product, tail: unwrap the head's result
+constexpr int FL_TWIST = 16;  // split truncated product, twisted quarter piece (mod x^(L'/4) - i)
 
 // Persistent kernel: each CTA copies the (p, L) stage tables into shared
 // memory once and then walks the batch with a grid stride.
@@ -686,8 +693,25 @@ conv_small_kernel(const ConvSmallParams P) {
 #pragma unroll
             for (int s = 0; s < 16; ++s) {
                 const int x = (s << (K - 4)) | t;
-                va[s] = (valid && x < P.z1) ? __ldcs(ga + x) : 0u;
-                vb[s] = (valid && x < P.z2) ? __ldcs(gb + x) : 0u;
+                if constexpr ((FL & FL_TWIST) != 0) {
+                    // a mod (x^L - i) (quarters folded with i^k), twisted by w_L'^x
+                    // into the ring of the cyclic L-point product
+                    auto fold4 = [&](const u32 *g, int z) {
+                        const u32 u0 = (valid && x < z) ? __ldcs(g + x) : 0u;
+                        const u32 u1 = (valid && x + L < z) ? __ldcs(g + x + L) : 0u;
+                        const u32 u2 = (valid && x + 2 * L < z) ? __ldcs(g + x + 2 * L) : 0u;
+                        const u32 u3 = (valid && x + 3 * L < z) ? __ldcs(g + x + 3 * L) : 0u;
+                        const u32 f = add_mod(sub_mod(u0, u2, P.p),
+                                              mul_shoup(sub_mod(u1, u3, P.p), P.qi, P.p), P.p);
+                        const uint2 w = __ldg(P.twq_f + x);
+                        return mul_shoup(f, w.x, w.y, P.p);
+                    };
+                    va[s] = fold4(ga, P.tz1);
+                    vb[s] = fold4(gb, P.tz2);
+                } else {
+                    va[s] = (valid && x < P.z1) ? __ldcs(ga + x) : 0u;
+                    vb[s] = (valid && x < P.z2) ? __ldcs(gb + x) : 0u;
+                }
                 if constexpr ((FL & FL_FOLD) != 0) {
                     if (valid && x + L < P.z1) va[s] = add_mod(va[s], __ldcs(ga + x + L), P.p);
                     if (valid && x + L < P.z2) vb[s] = add_mod(vb[s], __ldcs(gb + x + L), P.p);
@@ -779,7 +803,27 @@ conv_small_kernel(const ConvSmallParams P) {
             if (head + nb + t < P.n) gc[head + nb + t] = stg[head + nb + t];
         } else if (valid) {
             u32 *gc = P.c + row * P.ldc;
-            if constexpr ((FL & FL_WRAP) != 0) {
+            if constexpr ((FL & FL_TWIST) != 0) {
+                // c1 = c mod (x^L - i) (untwisted); c0 = c mod (x^(2L) - 1) from
+                // the head; c = c0 + (x^(2L) - 1) h with h = (c0 mod (x^L - i) - c1) / 2
+                u32 c0l[16], c0h[16];  // all loads in flight before the first store
+#pragma unroll
+                for (int s = 0; s < 16; ++s) {
+                    const int x = (s << (K - 4)) | t;
+                    c0l[s] = __ldcs(gc + x);
+                    c0h[s] = __ldcs(gc + x + L);
+                }
+#pragma unroll
+                for (int s = 0; s < 16; ++s) {
+                    const int x = (s << (K - 4)) | t;
+                    const uint2 w = __ldg(P.twq_i + x);
+                    const u32 c1 = mul_shoup(canon_t<AR>(va[s], P.p), w.x, w.y, P.p);
+                    const u32 f = add_mod(c0l[s], mul_shoup(c0h[s], P.qi, P.p), P.p);
+                    const u32 h = mul_shoup(sub_mod(f, c1, P.p), P.qhalf, P.p);
+                    __stcs(gc + x, sub_mod(c0l[s], h, P.p));
+                    if (x < P.wrap_m) __stcs(gc + P.wrap_off + x, h);
+                }
+            } else if constexpr ((FL & FL_WRAP) != 0) {
                 // c0 = c mod (x^(L/2) - 1) from the head launch holds c[x] +
                 // c[x + L/2] for x < m; the low product gives c[x]
                 u32 c0[16];  // all loads in flight before the first store

@@ -48,6 +48,7 @@ static cudaError_t launch_nt(const ConvSmallParams &P, cudaStream_t st) {
         if constexpr (NT == 16) {
             if (P.reduce || P.bulk_out || P.ready || (P.fold && P.wrap_m))
                 return cudaErrorInvalidValue;
+            if (P.twq_f) return launch_nt_fl<NT, AR, FL_TWIST>(P, st);
             return P.fold ? launch_nt_fl<NT, AR, FL_FOLD>(P, st)
                           : launch_nt_fl<NT, AR, FL_WRAP>(P, st);
         } else {

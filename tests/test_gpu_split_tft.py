@@ -51,8 +51,10 @@ def test_split_boundaries(orc, K):
     """K <= 14: fused head; K = 15, 16: four-step head (circular L/2-point
     product of the folded operands, plain column loads)."""
     L = 1 << K
-    for m in sorted({1, 2, 3, 7, L // 16 - 1, L // 16, L // 16 + 1, L // 8 - 1, L // 8}):
-        if m < 1 or m > min(L // 8, 4096):
+    twist = K in (13, 14)  # m in (L/8, L/4]: the twisted quarter piece
+    for m in sorted({1, 2, 3, 7, L // 16 - 1, L // 16, L // 16 + 1, L // 8 - 1, L // 8,
+                     L // 8 + 1, 3 * L // 16, L // 4 - 1, L // 4}):
+        if m < 1 or m > (L // 4 if twist else min(L // 8, 4096)):
             continue
         n = L // 2 + m
         for z1 in sorted({1, 2, (n + 1) // 2, m, L // 2, L // 2 + 1}):
@@ -70,7 +72,7 @@ def test_split_boundaries(orc, K):
 def test_split_strided_and_aligned(orc, p):
     for K in (11, 12, 13, 14, 15):
         L = 1 << K
-        for m in (5, min(L // 8, 4096)):
+        for m in (5, min(L // 8, 4096)) + ((L // 4,) if K in (13, 14) else ()):
             n = L // 2 + m
             z1 = (n + 1) // 2
             z2 = n + 1 - z1
@@ -81,7 +83,7 @@ def test_split_strided_and_aligned(orc, p):
 def test_split_all_p_minus_1(orc):
     for K in (8, 12, 14):
         L = 1 << K
-        for m in (1, L // 8):
+        for m in (1, L // 8) + ((L // 4,) if K == 14 else ()):
             n = L // 2 + m
             z1 = (n + 1) // 2
             z2 = n + 1 - z1
@@ -93,11 +95,11 @@ def test_split_all_p_minus_1(orc):
             assert np.array_equal(got, np.repeat(want, rows, axis=0)), (K, m)
 
 
-def test_split_not_taken_past_eighth(orc):
-    """m > L/8 keeps the single relaxed-truncation launch (fused sizes) or
-    the relaxed four-step passes."""
+def test_split_not_taken_past_quarter(orc):
+    """m > L/4 keeps a single launch (the complete transform at fused sizes)
+    or the relaxed four-step passes."""
     L = 4096
-    n = L // 2 + L // 8 + 1
+    n = L // 2 + L // 4 + 1
     z1 = (n + 1) // 2
     assert _check(orc, P2, z1, n + 1 - z1, 3, seed=5) == 1
     L = 1 << 17
