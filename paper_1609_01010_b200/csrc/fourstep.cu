@@ -488,7 +488,13 @@ mc_status fourstep_plan(int engine, const u32 *a, long long lda, int z1, const u
     FourParams &P = F->P;
     memset(&P, 0, sizeof(P));
     if ((s = get_twist(TL, &P.tw)) != MC_OK) return s;
-    if (twist_table_on(K) && (s = get_full_twist(TL, P.tw, KC, &P.twf, &P.twi)) != MC_OK)
+    // Full twist tables pay when several products share each table row (the
+    // row items of a chunk are row-major over its products); a single product
+    // reads every row once from DRAM, and forming the twists from the small
+    // power tables is faster there (config 5, one product per prime: 123.8 ->
+    // 121.2 us; config 4, 8 products: 1.063 ms with the tables, 1.166 without)
+    if (twist_table_on(K) && batch >= 2 &&
+        (s = get_full_twist(TL, P.tw, KC, &P.twf, &P.twi)) != MC_OK)
         return s;
     P.cs.p = p;
     memcpy(P.cs.mlev, TR->mlev, sizeof(P.cs.mlev));  // column-level ITFT constants
