@@ -466,17 +466,42 @@ __device__ __forceinline__ bool pass_active(int t) {
     else return gblock_of_pass<K, I>(t & ~31) < NT;  // warp-uniform
 }
 
+// Scope of an exchange between the layouts SBW (the wider one: higher slot
+// window) and a lower one.  Thread t holds in layout SBW the positions with
+// low bits t mod 2^SBW and high bits t >> SBW, and in any lower layout only
+// positions of the block (t >> SBW) << (SBW + 4): every exchange stays inside
+// aligned groups of 2^SBW threads.  With SBW <= 5 such a group lies in one
+// warp (a product's threads are contiguous and T is a power of two), so the
+// two CTA barriers of the exchange become warp barriers: the 4 -> 0 exchange
+// of every size, and every exchange of the sizes with T <= 32.  The warps of a
+// CTA then drift apart between the remaining CTA barriers, and one warp's
+// exchange overlaps the others' butterflies.  MC_WARP_EXCH=0: CTA barriers
+// everywhere (A/B).
+#ifndef MC_WARP_EXCH
+#define MC_WARP_EXCH 1
+#endif
+
+template <int SBW>
+constexpr bool exch_local() { return MC_WARP_EXCH && SBW <= 5; }
+
+template <bool LOCAL>
+__device__ __forceinline__ void exch_sync() {
+    if constexpr (LOCAL) mc_syncwarp();
+    else mc_sync();
+}
+
 template <int K, int NT, int I, int AR = 0, class TW = Tw>
 __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[16], u32 (&vb)[16],
                                                 int t, const ConvSmallParams &P, const TW &W) {
     if constexpr (I < Plan<K>::NP) {
         constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         constexpr int SB = Plan<K>::sb(I);
-        mc_sync();
+        constexpr bool LOCAL = exch_local<SBprev>();
+        exch_sync<LOCAL>();
         put<SBprev>(bufA, va, t);
         put<SBprev>(bufB, vb, t);
 #ifndef MC_RACE_SELFTEST  // self-test of the race-stress build: this barrier removed must fail
-        mc_sync();
+        exch_sync<LOCAL>();
 #endif
         get<SB>(bufA, va, t);
         get<SB>(bufB, vb, t);
@@ -529,11 +554,12 @@ __device__ __forceinline__ void inv_lower_chain(u32 *buf, u32 (&v)[16], int t,
     if constexpr (I >= 0) {
         constexpr int SB = Plan<K>::sb(I);
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
+        constexpr bool LOCAL = exch_local<SBnext>();
         if (pass_active<K, I, NT>(t))
             inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v, t, P, W);  // zeros stay zeros
-        mc_sync();
+        exch_sync<LOCAL>();
         put<SB>(buf, v, t);
-        mc_sync();
+        exch_sync<LOCAL>();
         get<SBnext>(buf, v, t);
         inv_lower_chain<K, NT, I - 1, AR, TW>(buf, v, t, P, W);
     }

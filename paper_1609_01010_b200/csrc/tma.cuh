@@ -29,6 +29,13 @@ __device__ __forceinline__ void mc_sync() {
     mc_perturb();
 }
 
+// Warp-scope barrier for the exchanges whose writers and readers share a warp
+// (conv_small.cuh exch_local): orders the warp's shared-memory accesses.
+__device__ __forceinline__ void mc_syncwarp() {
+    __syncwarp();
+    mc_perturb();
+}
+
 namespace mc {
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
