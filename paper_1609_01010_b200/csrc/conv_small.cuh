@@ -376,16 +376,24 @@ __device__ __forceinline__ void inv_top(u32 (&v)[16], int t, const ConvSmallPara
 // per buffer (swz).  LayCol<TC>: TC interleaved column transforms, element
 // (x, c) in row x of a TC-wide tile; rows are XOR-permuted so that the
 // 32/TC transform threads sharing a warp always hit distinct bank groups.
+// kCols: interleaved transforms per tile (thread index = t * kCols + c);
+// kThreads: threads of the CTA if its exchange groups may use named barriers
+// (exch_sync), else 0.
 struct LaySmall {
+    static constexpr int kCols = 1, kThreads = 0;
     __device__ __forceinline__ int operator()(int x) const { return swz(x); }
 };
 
 struct LayXf {  // standalone transforms: scalar accesses only (swz_xf)
+    static constexpr int kCols = 1, kThreads = 0;
     __device__ __forceinline__ int operator()(int x) const { return swz_xf(x); }
 };
 
-template <int TC>
+// CW: columns per thread (1, or 2: columns c and c + 1, c even, exchanged as
+// 8-byte words; kCols counts thread columns).
+template <int TC, int NTH = 0, int CW = 1>
 struct LayCol {
+    static constexpr int kCols = TC / CW, kThreads = NTH;
     int c;
     static constexpr int M = TC >= 32 ? 0 : 32 / TC - 1;
     __device__ __forceinline__ int operator()(int x) const { return (x ^ ((x >> 4) & M)) * TC + c; }
@@ -420,6 +428,28 @@ __device__ __forceinline__ void get(const u32 *buf, u32 (&v)[16], int t, Lay lay
     } else {
 #pragma unroll
         for (int s = 0; s < 16; ++s) v[s] = buf[lay(slot_pos<SB>(t, s))];
+    }
+}
+
+// Two interleaved column transforms per thread (LayCol with CW = 2): slot s of
+// columns c and c + 1 travels as one 8-byte word.
+template <int SB, class Lay>
+__device__ __forceinline__ void put2(u32 *buf, const u32 (&v0)[16], const u32 (&v1)[16], int t,
+                                     Lay lay) {
+    mc_perturb();
+#pragma unroll
+    for (int s = 0; s < 16; ++s)
+        *reinterpret_cast<uint2 *>(buf + lay(slot_pos<SB>(t, s))) = make_uint2(v0[s], v1[s]);
+}
+
+template <int SB, class Lay>
+__device__ __forceinline__ void get2(const u32 *buf, u32 (&v0)[16], u32 (&v1)[16], int t, Lay lay) {
+    mc_perturb();
+#pragma unroll
+    for (int s = 0; s < 16; ++s) {
+        const uint2 q = *reinterpret_cast<const uint2 *>(buf + lay(slot_pos<SB>(t, s)));
+        v0[s] = q.x;
+        v1[s] = q.y;
     }
 }
 
@@ -470,24 +500,34 @@ __device__ __forceinline__ bool pass_active(int t) {
 // window) and a lower one.  Thread t holds in layout SBW the positions with
 // low bits t mod 2^SBW and high bits t >> SBW, and in any lower layout only
 // positions of the block (t >> SBW) << (SBW + 4): every exchange stays inside
-// aligned groups of 2^SBW threads.  With SBW <= 5 such a group lies in one
-// warp (a product's threads are contiguous and T is a power of two), so the
-// two CTA barriers of the exchange become warp barriers: the 4 -> 0 exchange
-// of every size, and every exchange of the sizes with T <= 32.  The warps of a
-// CTA then drift apart between the remaining CTA barriers, and one warp's
-// exchange overlaps the others' butterflies.  MC_WARP_EXCH=0: CTA barriers
-// everywhere (A/B).
+// aligned groups of 2^SBW transform threads (times the TC interleaved columns
+// of a column tile), which are contiguous in threadIdx.  A group of GT <= 32
+// threads lies in one warp and synchronises with a warp barrier (the 4 -> 0
+// exchange of every row transform, every exchange of the sizes with T <= 32);
+// a larger group that is a proper part of the CTA uses its own named barrier
+// (bar.sync 1 + group, GT: the 8 -> 4 exchange at K = 13, the products of a
+// multi-product CTA, the 4 -> 0 exchange of a column tile).  The groups then
+// drift apart between the remaining CTA barriers, and one group's exchange
+// overlaps the others' butterflies.  NTH = threads of the CTA (0: unknown,
+// CTA barriers).  MC_WARP_EXCH=0: CTA barriers everywhere (A/B).
 #ifndef MC_WARP_EXCH
 #define MC_WARP_EXCH 1
 #endif
 
-template <int SBW>
-constexpr bool exch_local() { return MC_WARP_EXCH && SBW <= 5; }
+// threads of a fused-kernel / row-pass CTA at transform size 2^K (SmallCfg, RowCfg)
+template <int K>
+constexpr int small_threads() { return (1 << K) / 16 >= 128 ? (1 << K) / 16 : 128; }
 
-template <bool LOCAL>
+template <int GT, int NTH>
 __device__ __forceinline__ void exch_sync() {
-    if constexpr (LOCAL) mc_syncwarp();
-    else mc_sync();
+    if constexpr (MC_WARP_EXCH && GT <= 32) {
+        mc_syncwarp();
+    } else if constexpr (MC_WARP_EXCH && NTH > 0 && GT < NTH && GT % 32 == 0 && NTH / GT <= 15) {
+        asm volatile("bar.sync %0, %1;" ::"r"(1 + (int)threadIdx.x / GT), "n"(GT) : "memory");
+        mc_perturb();
+    } else {
+        mc_sync();
+    }
 }
 
 template <int K, int NT, int I, int AR = 0, class TW = Tw>
@@ -496,12 +536,12 @@ __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[
     if constexpr (I < Plan<K>::NP) {
         constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         constexpr int SB = Plan<K>::sb(I);
-        constexpr bool LOCAL = exch_local<SBprev>();
-        exch_sync<LOCAL>();
+        constexpr int GT = 1 << SBprev, NTH = small_threads<K>();
+        exch_sync<GT, NTH>();
         put<SBprev>(bufA, va, t);
         put<SBprev>(bufB, vb, t);
 #ifndef MC_RACE_SELFTEST  // self-test of the race-stress build: this barrier removed must fail
-        exch_sync<LOCAL>();
+        exch_sync<GT, NTH>();
 #endif
         get<SB>(bufA, va, t);
         get<SB>(bufB, vb, t);
@@ -554,12 +594,12 @@ __device__ __forceinline__ void inv_lower_chain(u32 *buf, u32 (&v)[16], int t,
     if constexpr (I >= 0) {
         constexpr int SB = Plan<K>::sb(I);
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
-        constexpr bool LOCAL = exch_local<SBnext>();
+        constexpr int GT = 1 << SBnext, NTH = small_threads<K>();
         if (pass_active<K, I, NT>(t))
             inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v, t, P, W);  // zeros stay zeros
-        exch_sync<LOCAL>();
+        exch_sync<GT, NTH>();
         put<SB>(buf, v, t);
-        exch_sync<LOCAL>();
+        exch_sync<GT, NTH>();
         get<SBnext>(buf, v, t);
         inv_lower_chain<K, NT, I - 1, AR, TW>(buf, v, t, P, W);
     }
@@ -573,9 +613,10 @@ __device__ __forceinline__ void fwd_lower_chain1(u32 *buf, u32 (&v)[16], int t,
     if constexpr (I < Plan<K>::NP) {
         constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         constexpr int SB = Plan<K>::sb(I);
-        mc_sync();
+        constexpr int GT = (1 << SBprev) * Lay::kCols;
+        exch_sync<GT, Lay::kThreads>();
         put<SBprev>(buf, v, t, lay);
-        mc_sync();
+        exch_sync<GT, Lay::kThreads>();
         get<SB>(buf, v, t, lay);
         if (NT >= 16 || gblock_of_pass<K, I>(t) < NT)
             fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v, t, P, W);
@@ -589,13 +630,54 @@ __device__ __forceinline__ void inv_lower_chain1(u32 *buf, u32 (&v)[16], int t,
     if constexpr (I >= 0) {
         constexpr int SB = Plan<K>::sb(I);
         constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
+        constexpr int GT = (1 << SBnext) * Lay::kCols;
         if (NT >= 16 || gblock_of_pass<K, I>(t) < NT)
             inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v, t, P, W);
-        mc_sync();
+        exch_sync<GT, Lay::kThreads>();
         put<SB>(buf, v, t, lay);
-        mc_sync();
+        exch_sync<GT, Lay::kThreads>();
         get<SBnext>(buf, v, t, lay);
         inv_lower_chain1<K, I - 1, Lay, NT, AR, TW>(buf, v, t, P, W, lay);
+    }
+}
+
+// Two columns per thread: the same passes on v0 and v1 (one set of twiddle
+// loads serves both), 8-byte exchanges.
+template <int K, int I, class Lay, int NT = 16, int AR = 0, class TW = Tw>
+__device__ __forceinline__ void fwd_lower_chain2(u32 *buf, u32 (&v0)[16], u32 (&v1)[16], int t,
+                                                 const ConvSmallParams &P, const TW &W, Lay lay) {
+    if constexpr (I < Plan<K>::NP) {
+        constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
+        constexpr int SB = Plan<K>::sb(I);
+        constexpr int GT = (1 << SBprev) * Lay::kCols;
+        exch_sync<GT, Lay::kThreads>();
+        put2<SBprev>(buf, v0, v1, t, lay);
+        exch_sync<GT, Lay::kThreads>();
+        get2<SB>(buf, v0, v1, t, lay);
+        if (NT >= 16 || gblock_of_pass<K, I>(t) < NT) {
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v0, t, P, W);
+            fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v1, t, P, W);
+        }
+        fwd_lower_chain2<K, I + 1, Lay, NT, AR, TW>(buf, v0, v1, t, P, W, lay);
+    }
+}
+
+template <int K, int I, class Lay, int NT = 16, int AR = 0, class TW = Tw>
+__device__ __forceinline__ void inv_lower_chain2(u32 *buf, u32 (&v0)[16], u32 (&v1)[16], int t,
+                                                 const ConvSmallParams &P, const TW &W, Lay lay) {
+    if constexpr (I >= 0) {
+        constexpr int SB = Plan<K>::sb(I);
+        constexpr int SBnext = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
+        constexpr int GT = (1 << SBnext) * Lay::kCols;
+        if (NT >= 16 || gblock_of_pass<K, I>(t) < NT) {
+            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v0, t, P, W);
+            inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v1, t, P, W);
+        }
+        exch_sync<GT, Lay::kThreads>();
+        put2<SB>(buf, v0, v1, t, lay);
+        exch_sync<GT, Lay::kThreads>();
+        get2<SBnext>(buf, v0, v1, t, lay);
+        inv_lower_chain2<K, I - 1, Lay, NT, AR, TW>(buf, v0, v1, t, P, W, lay);
     }
 }
 
@@ -608,6 +690,7 @@ struct SmallCfg {
     static constexpr int T = L / 16;
     static constexpr int PPC = T >= 128 ? 1 : 128 / T;  // products per CTA
     static constexpr int THREADS = T * PPC;
+    static_assert(THREADS == small_threads<K>(), "exch_sync group barriers assume this CTA size");
     static constexpr int MINB = THREADS >= 512 ? 1 : 2;  // CTAs per SM (register cap)
     // shared memory: forward + inverse stage tables, then 2 operand buffers
     // per product

@@ -31,6 +31,7 @@ struct RowCfg {
     static constexpr int T = C / 16;
     static constexpr int PPC = T >= 128 ? 1 : 128 / T;
     static constexpr int THREADS = T * PPC;
+    static_assert(THREADS == small_threads<KC>(), "exch_sync group barriers assume this CTA size");
     static constexpr int TM = (C - 1 + KC + 1) & ~1;  // merged-table entries (even)
     static constexpr int TABW = MC_ROW_TM ? TM : 2 * C;  // table entries in shared memory
     // with one row pair per CTA (PPC == 1) the next pair lands in a staging
@@ -427,7 +428,7 @@ static ColTma make_col_tma(const u32 *a, long long lda, long long z1, const u32 
     memset(&M, 0, sizeof(M));
     static const bool off = [] { const char *e = getenv("MC_NO_COL_TMA"); return e && *e; }();
     const long long C = 1ll << KC;
-    const int TC = 16384 >> KR;
+    const int TC = MC_COL_TILE >> KR;
     const int BR = std::min(1 << KR, 256);
     auto enc = tensor_map_encoder();
     if (off || !enc || KR < 6 || (z1 % C) || (z2 % C) || (lda % 4) || (ldb % 4) ||

@@ -48,8 +48,8 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_fwd
     }
     const int zrows = (int)((z + Ccols - 1) / Ccols);
     fwd_top<KR, NT, AR>(v, zrows, t, P.cs, W);
-    LayCol<C::TC> lay{c};
-    fwd_lower_chain1<KR, 0, LayCol<C::TC>, NT, AR>(tile, v, t, P.cs, W, lay);
+    LayCol<C::TC, C::THREADS> lay{c};
+    fwd_lower_chain1<KR, 0, LayCol<C::TC, C::THREADS>, NT, AR>(tile, v, t, P.cs, W, lay);
     constexpr int SB = last_sb<KR>();
 #pragma unroll
     for (int s = 0; s < 16; ++s) {
@@ -76,6 +76,37 @@ __device__ __forceinline__ void store_col(u32 *dst, const u32 (&v)[16], int t, l
 #pragma unroll
         for (int s = 0; s < 16; ++s)
             if (idx0 + s * SLOT < P.n) __stcs(base + s * SLOT, canon_t<AR>(v[s], P.cs.p));
+    }
+}
+
+// Two adjacent columns per thread (col even, both below the wrap of the
+// column rotation): 8-byte stores.  The output address of column col is
+// congruent to the tile column modulo 8 words (out_rot), so it is 8-byte
+// aligned.  A row's last position n - 1 may fall between the two columns.
+template <int KR, int KC, int NT, int AR>
+__device__ __forceinline__ void store_col2(u32 *dst, const u32 (&v0)[16], const u32 (&v1)[16],
+                                           int t, long long col, long long tile_maxcol,
+                                           const FourParams &P) {
+    using C = ColCfg<KR>;
+    constexpr long long Ccols = 1ll << KC;
+    constexpr long long SLOT = (long long)C::G * Ccols;
+    u32 *base = dst + (long long)t * Ccols + col;
+    const u32 p = P.cs.p;
+    if (15 * SLOT + (long long)(C::G - 1) * Ccols + tile_maxcol < P.n) {
+#pragma unroll
+        for (int s = 0; s < 16; ++s)
+            __stcs(reinterpret_cast<uint2 *>(base + s * SLOT),
+                   make_uint2(canon_t<AR>(v0[s], p), canon_t<AR>(v1[s], p)));
+    } else {
+        const long long idx0 = (long long)t * Ccols + col;
+#pragma unroll
+        for (int s = 0; s < 16; ++s) {
+            if (idx0 + s * SLOT + 1 < P.n)
+                __stcs(reinterpret_cast<uint2 *>(base + s * SLOT),
+                       make_uint2(canon_t<AR>(v0[s], p), canon_t<AR>(v1[s], p)));
+            else if (idx0 + s * SLOT < P.n)
+                __stcs(base + s * SLOT, canon_t<AR>(v0[s], p));
+        }
     }
 }
 
@@ -116,8 +147,8 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_inv
         const int row = slot_pos<SB>(t, s);
         v[s] = (NT >= 16 || (row >> (KR - 4)) < NT) ? src[(long long)row * Ccols + j0 + c] : 0u;
     }
-    LayCol<C::TC> lay{c};
-    inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, NT, AR>(tile, v, t, P.cs, W, lay);
+    LayCol<C::TC, C::THREADS> lay{c};
+    inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC, C::THREADS>, NT, AR>(tile, v, t, P.cs, W, lay);
     inv_top<KR, NT, AR>(v, t, P.cs, W);
     store_col<KR, KC, NT, AR>(dst, v, t, col, maxcol, P);
 }
@@ -127,11 +158,19 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_inv
 // 3-D tensor-map bulk loads into one of two shared buffers while the
 // previous tile is being transformed, so DRAM latency is off the critical
 // path and the 16 strided scalar loads per thread disappear.
-template <int KR, int KC, int NT, int AR = 0>
-__global__ void __launch_bounds__(1024, 1)
+// CW = 2: every thread transforms two adjacent columns (half the threads):
+// one set of twiddle loads and exchange addresses serves both, and the tile
+// reads, exchanges and spectrum stores move 8-byte words.
+#ifndef MC_COL_CW
+#define MC_COL_CW 1
+#endif
+
+template <int KR, int KC, int NT, int AR = 0, int CW = 1>
+__global__ void __launch_bounds__(ColCfg<KR>::THREADS / CW, ColCfg<KR>::TILE <= 8192 ? 2 : 1)
 col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
                    const __grid_constant__ CUtensorMap tb, int ntiles) {
     using C = ColCfg<KR>;
+    constexpr int THREADS = C::THREADS / CW;
     constexpr int BR = C::R < 256 ? C::R : 256;
     constexpr int NBOX = C::R / BR;
     constexpr long long Ccols = 1ll << KC;
@@ -141,11 +180,11 @@ col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
     u32 *buf0 = reinterpret_cast<u32 *>(tf_s + 2 * C::R);
     u32 *buf1 = buf0 + C::TILE;
     uint64_t *bar = reinterpret_cast<uint64_t *>(buf1 + C::TILE);
-    for (int i = threadIdx.x; i < C::R / 2; i += C::THREADS)
+    for (int i = threadIdx.x; i < C::R / 2; i += THREADS)
         reinterpret_cast<uint4 *>(tf_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_tf) + i);
     const Tw W{tf_s, tf_s};
-    const int c = threadIdx.x % C::TC;
-    const int t = threadIdx.x / C::TC;
+    const int c = CW * (threadIdx.x % (C::TC / CW));
+    const int t = threadIdx.x / (C::TC / CW);
     const u32 p = P.cs.p;
     if (threadIdx.x == 0) {
         mbar_init(bar, 1);
@@ -176,27 +215,50 @@ col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
             mbar_wait(bar, ph0);
             ph0 ^= 1;
         }
-        u32 v[16];
-#pragma unroll
-        for (int s = 0; s < 16; ++s) {  // plain row-major tile: conflict-free for this layout
-            u32 x = buf[(t + C::G * s) * C::TC + c];
-            if (P.reduce) x = mul_t<AR>(x, 1u, P.red_wp, p);
-            v[s] = x;
-        }
-        mc_sync();  // tile consumed; the other buffer is free since last iteration
-        if (threadIdx.x == 0 && tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, k ^ 1);
         const long long z = op ? P.z2 : P.z1;
         const int zrows = (int)((z + Ccols - 1) / Ccols);
-        fwd_top<KR, NT, AR>(v, zrows, t, P.cs, W);
-        LayCol<C::TC> lay{c};
-        fwd_lower_chain1<KR, 0, LayCol<C::TC>, NT, AR>(buf, v, t, P.cs, W, lay);
         u32 *dst = (op ? P.Bh : P.Ah) + (long long)pc * (Ccols << KR);
         const long long col = (long long)ct * C::TC + c;
         constexpr int SB = last_sb<KR>();
+        if constexpr (CW == 2) {
+            u32 v0[16], v1[16];
 #pragma unroll
-        for (int s = 0; s < 16; ++s) {
-            const int row = slot_pos<SB>(t, s);
-            if (NT >= 16 || (row >> (KR - 4)) < NT) dst[(long long)row * Ccols + col] = v[s];
+            for (int s = 0; s < 16; ++s) {
+                const uint2 q = *reinterpret_cast<const uint2 *>(buf + (t + C::G * s) * C::TC + c);
+                v0[s] = P.reduce ? mul_t<AR>(q.x, 1u, P.red_wp, p) : q.x;
+                v1[s] = P.reduce ? mul_t<AR>(q.y, 1u, P.red_wp, p) : q.y;
+            }
+            mc_sync();  // tile consumed; the other buffer is free since last iteration
+            if (threadIdx.x == 0 && tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, k ^ 1);
+            fwd_top<KR, NT, AR>(v0, zrows, t, P.cs, W);
+            fwd_top<KR, NT, AR>(v1, zrows, t, P.cs, W);
+            LayCol<C::TC, THREADS, 2> lay{c};
+            fwd_lower_chain2<KR, 0, LayCol<C::TC, THREADS, 2>, NT, AR>(buf, v0, v1, t, P.cs, W, lay);
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const int row = slot_pos<SB>(t, s);
+                if (NT >= 16 || (row >> (KR - 4)) < NT)
+                    *reinterpret_cast<uint2 *>(dst + (long long)row * Ccols + col) =
+                        make_uint2(v0[s], v1[s]);
+            }
+        } else {
+            u32 v[16];
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {  // plain row-major tile: conflict-free for this layout
+                u32 x = buf[(t + C::G * s) * C::TC + c];
+                if (P.reduce) x = mul_t<AR>(x, 1u, P.red_wp, p);
+                v[s] = x;
+            }
+            mc_sync();  // tile consumed; the other buffer is free since last iteration
+            if (threadIdx.x == 0 && tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, k ^ 1);
+            fwd_top<KR, NT, AR>(v, zrows, t, P.cs, W);
+            LayCol<C::TC, THREADS> lay{c};
+            fwd_lower_chain1<KR, 0, LayCol<C::TC, THREADS>, NT, AR>(buf, v, t, P.cs, W, lay);
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const int row = slot_pos<SB>(t, s);
+                if (NT >= 16 || (row >> (KR - 4)) < NT) dst[(long long)row * Ccols + col] = v[s];
+            }
         }
         k ^= 1;
     }
@@ -217,10 +279,12 @@ struct ColInvAsync {
     }
 };
 
-template <int KR, int KC, int NT, int AR>
-__global__ void __launch_bounds__(1024, 1) col_inv_async_kernel(const FourParams P, int ntiles) {
+template <int KR, int KC, int NT, int AR, int CW = 1>
+__global__ void __launch_bounds__(ColCfg<KR>::THREADS / CW, ColCfg<KR>::TILE <= 8192 ? 2 : 1)
+col_inv_async_kernel(const FourParams P, int ntiles) {
     using C = ColCfg<KR>;
     using A = ColInvAsync<KR>;
+    constexpr int THREADS = C::THREADS / CW;
     constexpr long long Ccols = 1ll << KC;
     constexpr int CT = (1 << KC) / C::TC;
     constexpr int CHUNKS = C::TC / 4;     // 16-byte chunks per row
@@ -229,20 +293,20 @@ __global__ void __launch_bounds__(1024, 1) col_inv_async_kernel(const FourParams
     uint2 *tf_s = reinterpret_cast<uint2 *>(smem_raw);
     uint2 *ti_s = tf_s + C::R;
     u32 *bufs = reinterpret_cast<u32 *>(tf_s + 2 * C::R);
-    for (int i = threadIdx.x; i < C::R / 2; i += C::THREADS) {
+    for (int i = threadIdx.x; i < C::R / 2; i += THREADS) {
         reinterpret_cast<uint4 *>(ti_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_ti) + i);
         if (NT < 16)
             reinterpret_cast<uint4 *>(tf_s)[i] =
                 __ldg(reinterpret_cast<const uint4 *>(P.col_tf) + i);
     }
     const Tw W{tf_s, ti_s};
-    const int c = threadIdx.x % C::TC;
-    const int t = threadIdx.x / C::TC;
+    const int c = CW * (threadIdx.x % (C::TC / CW));
+    const int t = threadIdx.x / (C::TC / CW);
     auto issue = [&](int tile, int k) {  // every thread: its share of the tile's chunks
         const int ct = tile % CT, pc = tile / CT;
         const u32 *src = P.Ah + (long long)pc * (Ccols << KR) + (long long)ct * C::TC;
         u32 *dst = bufs + k * A::BUFW;
-        for (int q = threadIdx.x; q < NR * CHUNKS; q += C::THREADS) {
+        for (int q = threadIdx.x; q < NR * CHUNKS; q += THREADS) {
             const int row = q / CHUNKS, ch = q % CHUNKS;
             const u32 *g = src + (long long)row * Ccols + 4 * ch;
             const u32 sa = smem_u32(dst + A::off(row) + 4 * ch);
@@ -257,23 +321,51 @@ __global__ void __launch_bounds__(1024, 1) col_inv_async_kernel(const FourParams
         u32 *buf = bufs + k * A::BUFW;
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         mc_sync();
-        u32 v[16];
         constexpr int SB = last_sb<KR>();
-#pragma unroll
-        for (int s = 0; s < 16; ++s) {
-            const int row = slot_pos<SB>(t, s);
-            v[s] = (NT >= 16 || (row >> (KR - 4)) < NT) ? buf[A::off(row) + c] : 0u;
-        }
-        mc_sync();  // tile consumed; the other buffer is free
-        if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, k ^ 1);
-        LayCol<C::TC> lay{c};
-        inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, NT, AR>(buf, v, t, P.cs, W, lay);
-        inv_top<KR, NT, AR>(v, t, P.cs, W);
         u32 *dst = P.c + (P.prod0 + pc) * P.ldc;
         const int rot = out_rot(P, P.prod0 + pc);  // scratch column j = spectrum column j - rot
         const long long j0 = (long long)ct * C::TC;
         const long long col = (j0 + c - rot) & (Ccols - 1);
-        store_col<KR, KC, NT, AR>(dst, v, t, col, j0 >= rot ? j0 - rot + C::TC - 1 : Ccols - 1, P);
+        const long long maxcol = j0 >= rot ? j0 - rot + C::TC - 1 : Ccols - 1;
+        if constexpr (CW == 2) {
+            u32 v0[16], v1[16];
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const int row = slot_pos<SB>(t, s);
+                const uint2 q = (NT >= 16 || (row >> (KR - 4)) < NT)
+                                    ? *reinterpret_cast<const uint2 *>(buf + A::off(row) + c)
+                                    : make_uint2(0u, 0u);
+                v0[s] = q.x;
+                v1[s] = q.y;
+            }
+            mc_sync();  // tile consumed; the other buffer is free
+            if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, k ^ 1);
+            LayCol<C::TC, THREADS, 2> lay{c};
+            inv_lower_chain2<KR, Plan<KR>::NP - 1, LayCol<C::TC, THREADS, 2>, NT, AR>(buf, v0, v1, t,
+                                                                                     P.cs, W, lay);
+            inv_top<KR, NT, AR>(v0, t, P.cs, W);
+            inv_top<KR, NT, AR>(v1, t, P.cs, W);
+            if (j0 >= rot) {  // tile-uniform: the pair (col, col + 1) does not straddle the wrap
+                store_col2<KR, KC, NT, AR>(dst, v0, v1, t, col, maxcol, P);
+            } else {
+                store_col<KR, KC, NT, AR>(dst, v0, t, col, maxcol, P);
+                store_col<KR, KC, NT, AR>(dst, v1, t, (col + 1) & (Ccols - 1), maxcol, P);
+            }
+        } else {
+            u32 v[16];
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const int row = slot_pos<SB>(t, s);
+                v[s] = (NT >= 16 || (row >> (KR - 4)) < NT) ? buf[A::off(row) + c] : 0u;
+            }
+            mc_sync();  // tile consumed; the other buffer is free
+            if (tile + (int)gridDim.x < ntiles) issue(tile + gridDim.x, k ^ 1);
+            LayCol<C::TC, THREADS> lay{c};
+            inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC, THREADS>, NT, AR>(buf, v, t, P.cs, W,
+                                                                                  lay);
+            inv_top<KR, NT, AR>(v, t, P.cs, W);
+            store_col<KR, KC, NT, AR>(dst, v, t, col, maxcol, P);
+        }
         k ^= 1;
     }
 }
@@ -281,17 +373,18 @@ __global__ void __launch_bounds__(1024, 1) col_inv_async_kernel(const FourParams
 template <int KR, int KC, int NT, int AR>
 static cudaError_t launch_inv_async(const FourParams &P, cudaStream_t st) {
     using C = ColCfg<KR>;
+    constexpr int CW = MC_COL_CW;
     static bool ready = false;
     if (!ready) {
-        cudaError_t e = prep_kernel(col_inv_async_kernel<KR, KC, NT, AR>, ColInvAsync<KR>::SMEM,
-                                    C::THREADS, nullptr);
+        cudaError_t e = prep_kernel(col_inv_async_kernel<KR, KC, NT, AR, CW>, ColInvAsync<KR>::SMEM,
+                                    C::THREADS / CW, nullptr);
         if (e != cudaSuccess) return e;
         ready = true;
     }
     const int ntiles = (int)((1ll << KC) / C::TC) * P.chunk;
-    const int grid = std::min(ntiles, sm_count());
-    col_inv_async_kernel<KR, KC, NT, AR>
-        <<<grid, C::THREADS, ColInvAsync<KR>::SMEM, st>>>(P, ntiles);
+    const int grid = std::min(ntiles, (C::TILE <= 8192 ? 2 : 1) * sm_count());
+    col_inv_async_kernel<KR, KC, NT, AR, CW>
+        <<<grid, C::THREADS / CW, ColInvAsync<KR>::SMEM, st>>>(P, ntiles);
     return cudaGetLastError();
 }
 
@@ -305,16 +398,19 @@ static bool col_inv_async_on() {
 template <int KR, int KC, int NT, int AR>
 static cudaError_t launch_fwd_tma(const FourParams &P, const ColTma &M, cudaStream_t st) {
     using C = ColCfg<KR>;
+    constexpr int CW = MC_COL_CW;
     constexpr int SMEM = 2 * C::R * 8 + 2 * C::TILE * 4 + 64;
     static bool ready = false;
     if (!ready) {
-        cudaError_t e = prep_kernel(col_fwd_tma_kernel<KR, KC, NT, AR>, SMEM, C::THREADS, nullptr);
+        cudaError_t e =
+            prep_kernel(col_fwd_tma_kernel<KR, KC, NT, AR, CW>, SMEM, C::THREADS / CW, nullptr);
         if (e != cudaSuccess) return e;
         ready = true;
     }
     const int ntiles = (int)((1ll << KC) / C::TC) * 2 * P.chunk;
-    const int grid = std::min(ntiles, sm_count());
-    col_fwd_tma_kernel<KR, KC, NT, AR><<<grid, C::THREADS, SMEM, st>>>(P, M.ma, M.mb, ntiles);
+    const int grid = std::min(ntiles, (C::TILE <= 8192 ? 2 : 1) * sm_count());
+    col_fwd_tma_kernel<KR, KC, NT, AR, CW>
+        <<<grid, C::THREADS / CW, SMEM, st>>>(P, M.ma, M.mb, ntiles);
     return cudaGetLastError();
 }
 
@@ -322,7 +418,7 @@ template <int KR, int KC, int NT, int AR = 0>
 static cudaError_t launch_one(const FourParams &P, bool fwd, cudaStream_t st,
                               const ColTma *tma) {
     // bulk-copy / async variants need >= 16-byte tile rows (TC >= 4, KR <= 12)
-    if constexpr (KR >= 6 && ColCfg<KR>::TILE == 16384 && ColCfg<KR>::TC >= 4) {
+    if constexpr (KR >= 6 && ColCfg<KR>::TILE >= 8192 && ColCfg<KR>::TC >= 4) {
         if (fwd && tma && tma->ok) return launch_fwd_tma<KR, KC, NT, AR>(P, *tma, st);
         if (!fwd && col_inv_async_on()) return launch_inv_async<KR, KC, NT, AR>(P, st);
     }

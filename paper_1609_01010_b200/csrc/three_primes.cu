@@ -60,9 +60,13 @@ __device__ __forceinline__ void inv3_column(const Inv3Params &Q, u32 *buf, const
 #pragma unroll
     for (int s = 0; s < 16; ++s) v[s] = buf[C::off(slot_pos<SB>(t, s)) + c];
     const Tw W{ti_s, ti_s};  // complete transforms: the forward table is never read
-    LayCol<C::TC> lay{c};
-    // the chain's first barrier orders these reads before the exchange writes
-    inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC>, 16, AR>(buf, v, t, Q.cs[K3], W, lay);
+    LayCol<C::TC, C::THREADS> lay{c};
+    // Every thread has read its landed values before any exchange write: the
+    // landing layout (padded rows) and the exchange layout place a block's rows
+    // at different addresses, and the chain's first exchange only synchronises
+    // its own thread group (exch_sync).
+    mc_sync();
+    inv_lower_chain1<KR, Plan<KR>::NP - 1, LayCol<C::TC, C::THREADS>, 16, AR>(buf, v, t, Q.cs[K3], W, lay);
     inv_top<KR, 16, AR>(v, t, Q.cs[K3], W);
 #pragma unroll
     for (int s = 0; s < 16; ++s) v[s] = canon_t<AR>(v[s], Q.cs[K3].p);
