@@ -423,12 +423,12 @@ static PFN_cuTensorMapEncodeTiled_v12000 tensor_map_encoder() {
 }
 
 static ColTma make_col_tma(const u32 *a, long long lda, long long z1, const u32 *b, long long ldb,
-                          long long z2, long long batch, int KC, int KR) {
+                          long long z2, long long batch, int KC, int KR, int tile) {
     ColTma M;
     memset(&M, 0, sizeof(M));
     static const bool off = [] { const char *e = getenv("MC_NO_COL_TMA"); return e && *e; }();
     const long long C = 1ll << KC;
-    const int TC = MC_COL_TILE >> KR;
+    const int TC = tile >> KR;
     const int BR = std::min(1 << KR, 256);
     auto enc = tensor_map_encoder();
     if (off || !enc || KR < 6 || (z1 % C) || (z2 % C) || (lda % 4) || (ldb % 4) ||
@@ -456,6 +456,16 @@ static cudaError_t launch_rows_any(int KC, int KR, const FourParams &P, cudaStre
         case 13: return launch_rows<13>(P, KR, st);
         default: return cudaErrorInvalidValue;
     }
+}
+
+// scratch budget per chunk (default 512 MiB: bigger launches beat L2 residency,
+// the four-step passes are integer-pipe bound; profiles/r01/README.md)
+static long long scratch_budget_words() {
+    static const long long budget_words = [] {
+        const char *e = getenv("MC_FOURSTEP_SCRATCH_MB");
+        return (e ? atoll(e) : 512ll) << 18;  // MiB -> 32-bit words
+    }();
+    return budget_words;
 }
 
 mc_status fourstep_plan(int engine, const u32 *a, long long lda, int z1, const u32 *b,
@@ -541,7 +551,16 @@ mc_status fourstep_plan(int engine, const u32 *a, long long lda, int z1, const u
     F->NT = NT;
     F->L = L;
     F->batch = batch;
-    F->tma = make_col_tma(a, lda, P.z1, b, ldb, P.z2, batch, KC, KR);
+    // narrower column tiles when one chunk's spectra (2L words per product)
+    // stay in L2; MC_SMALL_COL_TILES=0/1 forces (A/B)
+    {
+        const long long chunk = std::max(1ll, std::min(batch, scratch_budget_words() / (2 * L)));
+        P.small_tiles = NT == 16 && KR <= 11 && 8 * L * chunk <= (16ll << 20);
+        if (const char *f = getenv("MC_SMALL_COL_TILES"))
+            if (*f) P.small_tiles = atoi(f) && NT == 16 && KR <= 11;
+    }
+    F->tma = make_col_tma(a, lda, P.z1, b, ldb, P.z2, batch, KC, KR,
+                          P.small_tiles ? kSmallColTile : MC_COL_TILE);
     return MC_OK;
 }
 
@@ -584,13 +603,7 @@ mc_status fourstep_conv(int engine, const u32 *a, long long lda, int z1, const u
         return levels_conv(a, lda, z1, b, ldb, z2, c, ldc, batch, p, F.K,
                            circ_log2L >= 0 ? (1ll << circ_log2L) : (long long)z1 + z2 - 1, st);
     const long long L = F.L;
-    // scratch budget per chunk (default 512 MiB: bigger launches beat L2 residency,
-    // the four-step passes are integer-pipe bound; profiles/r01/README.md)
-    static const long long budget_words = [] {
-        const char *e = getenv("MC_FOURSTEP_SCRATCH_MB");
-        return (e ? atoll(e) : 512ll) << 18;  // MiB -> 32-bit words
-    }();
-    const long long chunk = std::max(1ll, std::min(batch, budget_words / (2 * L)));
+    const long long chunk = std::max(1ll, std::min(batch, scratch_budget_words() / (2 * L)));
     u32 *scratch = nullptr;
     keep_pool_memory();
     MC_CUDA_CHECK(cudaMallocAsync(&scratch, sizeof(u32) * 2 * L * chunk, st));

@@ -165,11 +165,11 @@ __global__ void __launch_bounds__(ColCfg<KR>::THREADS, ColCfg<KR>::MINB) col_inv
 #define MC_COL_CW 1
 #endif
 
-template <int KR, int KC, int NT, int AR = 0, int CW = 1>
-__global__ void __launch_bounds__(ColCfg<KR>::THREADS / CW, ColCfg<KR>::TILE <= 8192 ? 2 : 1)
+template <int KR, int KC, int NT, int AR = 0, int CW = 1, int TL = MC_COL_TILE>
+__global__ void __launch_bounds__(ColCfg<KR, TL>::THREADS / CW, TL <= 8192 ? 2 : 1)
 col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
                    const __grid_constant__ CUtensorMap tb, int ntiles) {
-    using C = ColCfg<KR>;
+    using C = ColCfg<KR, TL>;
     constexpr int THREADS = C::THREADS / CW;
     constexpr int BR = C::R < 256 ? C::R : 256;
     constexpr int NBOX = C::R / BR;
@@ -269,21 +269,21 @@ col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
 // scalar loads) into the other of two shared buffers while this tile is
 // transformed.  Landing layout: row r at r*TC + (r/16)*8 words, which makes
 // the first read (rows 16t + s, the last forward pass's layout) conflict-free.
-template <int KR>
+template <int KR, int TL = MC_COL_TILE>
 struct ColInvAsync {
     static constexpr int PADW = 8;  // words of padding per 16 rows
-    static constexpr int BUFW = ColCfg<KR>::TILE + (ColCfg<KR>::R / 16) * PADW;
-    static constexpr int SMEM = 2 * ColCfg<KR>::R * 8 + 2 * BUFW * 4;
+    static constexpr int BUFW = ColCfg<KR, TL>::TILE + (ColCfg<KR, TL>::R / 16) * PADW;
+    static constexpr int SMEM = 2 * ColCfg<KR, TL>::R * 8 + 2 * BUFW * 4;
     __device__ static __forceinline__ int off(int row) {
-        return row * ColCfg<KR>::TC + (row >> 4) * PADW;
+        return row * ColCfg<KR, TL>::TC + (row >> 4) * PADW;
     }
 };
 
-template <int KR, int KC, int NT, int AR, int CW = 1>
-__global__ void __launch_bounds__(ColCfg<KR>::THREADS / CW, ColCfg<KR>::TILE <= 8192 ? 2 : 1)
+template <int KR, int KC, int NT, int AR, int CW = 1, int TL = MC_COL_TILE>
+__global__ void __launch_bounds__(ColCfg<KR, TL>::THREADS / CW, TL <= 8192 ? 2 : 1)
 col_inv_async_kernel(const FourParams P, int ntiles) {
-    using C = ColCfg<KR>;
-    using A = ColInvAsync<KR>;
+    using C = ColCfg<KR, TL>;
+    using A = ColInvAsync<KR, TL>;
     constexpr int THREADS = C::THREADS / CW;
     constexpr long long Ccols = 1ll << KC;
     constexpr int CT = (1 << KC) / C::TC;
@@ -370,21 +370,20 @@ col_inv_async_kernel(const FourParams P, int ntiles) {
     }
 }
 
-template <int KR, int KC, int NT, int AR>
+template <int KR, int KC, int NT, int AR, int CW = MC_COL_CW, int TL = MC_COL_TILE>
 static cudaError_t launch_inv_async(const FourParams &P, cudaStream_t st) {
-    using C = ColCfg<KR>;
-    constexpr int CW = MC_COL_CW;
+    using C = ColCfg<KR, TL>;
     static bool ready = false;
     if (!ready) {
-        cudaError_t e = prep_kernel(col_inv_async_kernel<KR, KC, NT, AR, CW>, ColInvAsync<KR>::SMEM,
-                                    C::THREADS / CW, nullptr);
+        cudaError_t e = prep_kernel(col_inv_async_kernel<KR, KC, NT, AR, CW, TL>,
+                                    ColInvAsync<KR, TL>::SMEM, C::THREADS / CW, nullptr);
         if (e != cudaSuccess) return e;
         ready = true;
     }
     const int ntiles = (int)((1ll << KC) / C::TC) * P.chunk;
     const int grid = std::min(ntiles, (C::TILE <= 8192 ? 2 : 1) * sm_count());
-    col_inv_async_kernel<KR, KC, NT, AR, CW>
-        <<<grid, C::THREADS / CW, ColInvAsync<KR>::SMEM, st>>>(P, ntiles);
+    col_inv_async_kernel<KR, KC, NT, AR, CW, TL>
+        <<<grid, C::THREADS / CW, ColInvAsync<KR, TL>::SMEM, st>>>(P, ntiles);
     return cudaGetLastError();
 }
 
@@ -395,21 +394,20 @@ static bool col_inv_async_on() {
     return on;
 }
 
-template <int KR, int KC, int NT, int AR>
+template <int KR, int KC, int NT, int AR, int CW = MC_COL_CW, int TL = MC_COL_TILE>
 static cudaError_t launch_fwd_tma(const FourParams &P, const ColTma &M, cudaStream_t st) {
-    using C = ColCfg<KR>;
-    constexpr int CW = MC_COL_CW;
+    using C = ColCfg<KR, TL>;
     constexpr int SMEM = 2 * C::R * 8 + 2 * C::TILE * 4 + 64;
     static bool ready = false;
     if (!ready) {
         cudaError_t e =
-            prep_kernel(col_fwd_tma_kernel<KR, KC, NT, AR, CW>, SMEM, C::THREADS / CW, nullptr);
+            prep_kernel(col_fwd_tma_kernel<KR, KC, NT, AR, CW, TL>, SMEM, C::THREADS / CW, nullptr);
         if (e != cudaSuccess) return e;
         ready = true;
     }
     const int ntiles = (int)((1ll << KC) / C::TC) * 2 * P.chunk;
     const int grid = std::min(ntiles, (C::TILE <= 8192 ? 2 : 1) * sm_count());
-    col_fwd_tma_kernel<KR, KC, NT, AR, CW>
+    col_fwd_tma_kernel<KR, KC, NT, AR, CW, TL>
         <<<grid, C::THREADS / CW, SMEM, st>>>(P, M.ma, M.mb, ntiles);
     return cudaGetLastError();
 }
@@ -419,6 +417,15 @@ static cudaError_t launch_one(const FourParams &P, bool fwd, cudaStream_t st,
                               const ColTma *tma) {
     // bulk-copy / async variants need >= 16-byte tile rows (TC >= 4, KR <= 12)
     if constexpr (KR >= 6 && ColCfg<KR>::TILE >= 8192 && ColCfg<KR>::TC >= 4) {
+        // complete transforms on L2-resident chunks: narrower tiles (FourParams::small_tiles)
+        if constexpr (NT == 16 && ColCfg<KR, kSmallColTile>::TC >= 4) {
+            if (P.small_tiles) {
+                if (fwd && tma && tma->ok)
+                    return launch_fwd_tma<KR, KC, NT, AR, 2, kSmallColTile>(P, *tma, st);
+                if (!fwd && col_inv_async_on())
+                    return launch_inv_async<KR, KC, NT, AR, 2, kSmallColTile>(P, st);
+            }
+        }
         if (fwd && tma && tma->ok) return launch_fwd_tma<KR, KC, NT, AR>(P, *tma, st);
         if (!fwd && col_inv_async_on()) return launch_inv_async<KR, KC, NT, AR>(P, st);
     }

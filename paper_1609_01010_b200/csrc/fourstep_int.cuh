@@ -42,7 +42,14 @@ struct FourParams {
     const uint2 *twf, *twi;
     int row_prefetch;  // L2 bulk prefetch of the next row (the row pass's data exceeds L2)
     int fold;  // split truncated product head: operands longer than L fold x + L onto x
+    // Column passes on 8K-word tiles, two columns per thread, two CTAs per SM
+    // (kSmallColTile) instead of 16K-word tiles: chosen when a chunk's spectra
+    // stay in L2, where the 16-byte row segments of the narrower tiles cost
+    // nothing (config 5: 121.0 -> 117.0 us; config 4, DRAM-resident: 1.04 -> 1.44 ms)
+    int small_tiles;
 };
+
+constexpr int kSmallColTile = 8192;
 
 // Column rotation of the product spectrum.  The row pass writes spectrum
 // column x of (global) product g to scratch column (x + rot) mod C with rot =
@@ -79,10 +86,10 @@ __device__ __forceinline__ u32 shoup_comp(u32 w, u32 p, double two32_over_p) {
 // transform per R/16 threads.  16K-word tiles (1024 threads, 1 CTA/SM)
 // measured faster than 8K tiles with 2 CTAs/SM (narrower row segments cost
 // more than the load/compute overlap gained).
-template <int KR>
+template <int KR, int TL = MC_COL_TILE>
 struct ColCfg {
     static constexpr int R = 1 << KR;
-    static constexpr int TILE = MC_COL_TILE;
+    static constexpr int TILE = TL;
     static constexpr int TC = TILE >> KR;  // columns per tile
     static constexpr int THREADS = TILE / 16;
     static constexpr int G = R / 16;
