@@ -530,14 +530,30 @@ __device__ __forceinline__ void exch_sync() {
     }
 }
 
-template <int K, int NT, int I, int AR = 0, class TW = Tw>
+// The barrier BEFORE an exchange's stores (write-after-read) is only needed
+// when other threads may still be reading the locations a thread is about to
+// write.  Inside a chain every put<SB> rewrites exactly the positions the same
+// thread last read with get<SB> (the previous exchange of that buffer, or for
+// the inverse chain's first exchange the forward chain's last), so no other
+// thread ever read them since they were last written: these barriers are
+// dropped (MC_WAR_SYNC=1 keeps them, A/B).  The first forward exchange stores
+// the top-pass layout: bufA was last read in that layout by the previous
+// product's inverse (own positions again), bufB by the previous product's
+// forward chain, with the group barriers of the whole inverse chain in
+// between; only a launch whose epilogue reuses bufA as a bulk-store staging
+// area (FL_HOST) needs it (FS = true).
+#ifndef MC_WAR_SYNC
+#define MC_WAR_SYNC 0
+#endif
+
+template <int K, int NT, int I, int AR = 0, class TW = Tw, bool FS = true>
 __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[16], u32 (&vb)[16],
                                                 int t, const ConvSmallParams &P, const TW &W) {
     if constexpr (I < Plan<K>::NP) {
         constexpr int SBprev = (I == 0) ? (K - 4) : Plan<K>::sb(I - 1);
         constexpr int SB = Plan<K>::sb(I);
         constexpr int GT = 1 << SBprev, NTH = small_threads<K>();
-        exch_sync<GT, NTH>();
+        if constexpr (MC_WAR_SYNC || (I == 0 && FS)) exch_sync<GT, NTH>();
         put<SBprev>(bufA, va, t);
         put<SBprev>(bufB, vb, t);
 #ifndef MC_RACE_SELFTEST  // self-test of the race-stress build: this barrier removed must fail
@@ -551,7 +567,7 @@ __device__ __forceinline__ void fwd_lower_chain(u32 *bufA, u32 *bufB, u32 (&va)[
             fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(va, t, P, W);
             fwd_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(vb, t, P, W);
         }
-        fwd_lower_chain<K, NT, I + 1, AR, TW>(bufA, bufB, va, vb, t, P, W);
+        fwd_lower_chain<K, NT, I + 1, AR, TW, FS>(bufA, bufB, va, vb, t, P, W);
     }
 }
 
@@ -597,7 +613,7 @@ __device__ __forceinline__ void inv_lower_chain(u32 *buf, u32 (&v)[16], int t,
         constexpr int GT = 1 << SBnext, NTH = small_threads<K>();
         if (pass_active<K, I, NT>(t))
             inv_lower<K, Plan<K>::lo(I), Plan<K>::hi(I), SB, AR, TW>(v, t, P, W);  // zeros stay zeros
-        exch_sync<GT, NTH>();
+        if constexpr (MC_WAR_SYNC) exch_sync<GT, NTH>();
         put<SB>(buf, v, t);
         exch_sync<GT, NTH>();
         get<SBnext>(buf, v, t);
@@ -852,7 +868,7 @@ conv_small_kernel(const ConvSmallParams P) {
             // first exchange (after the barrier inside the chain) reuses bufA
             if ((FL & FL_HOST) && C::PPC == 1 && P.bulk_out && threadIdx.x == 0)
                 bulk_wait_read_all();
-            fwd_lower_chain<K, NT, 0, AR>(bufA, bufB, va, vb, t, P, W);
+            fwd_lower_chain<K, NT, 0, AR, Tw, (FL & FL_HOST) != 0>(bufA, bufB, va, vb, t, P, W);
         }
 
         // pointwise product in the last pass's layout, L^-1 folded in

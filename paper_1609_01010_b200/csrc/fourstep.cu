@@ -159,7 +159,7 @@ row_conv_kernel(const FourParams P, int KR) {
             }
             fwd_top<KC, 16, AR>(va, Cn, t, P.cs, W);
             fwd_top<KC, 16, AR>(vb, Cn, t, P.cs, W);
-            fwd_lower_chain<KC, 16, 0, AR>(bufA, bufB, va, vb, t, P.cs, W);
+            fwd_lower_chain<KC, 16, 0, AR, std::remove_const_t<decltype(W)>, false>(bufA, bufB, va, vb, t, P.cs, W);
 #pragma unroll
             for (int s = 0; s < 16; ++s) va[s] = mont_mul(va[s], vb[s], p, P.cs.pinv);
             inv_lower_chain<KC, 16, Plan<KC>::NP - 1, AR>(bufA, va, t, P.cs, W);
@@ -206,7 +206,7 @@ row_conv_kernel(const FourParams P, int KR) {
         }
         fwd_top<KC, 16, AR>(va, Cn, t, P.cs, W);
         fwd_top<KC, 16, AR>(vb, Cn, t, P.cs, W);
-        fwd_lower_chain<KC, 16, 0, AR>(bufA, bufB, va, vb, t, P.cs, W);
+        fwd_lower_chain<KC, 16, 0, AR, std::remove_const_t<decltype(W)>, false>(bufA, bufB, va, vb, t, P.cs, W);
 #pragma unroll
         for (int s = 0; s < 16; ++s)
             va[s] = mul_inv_t<AR>(mont_mul(va[s], vb[s], p, P.cs.pinv), P.cs.linv_mont, p);
