@@ -66,14 +66,52 @@ row_conv_kernel(const FourParams P, int KR) {
     u32 *bufA = reinterpret_cast<u32 *>(tm_s + RC::TABW) + grp * (2 * Cn + 64);
     u32 *bufB = bufA + Cn;
     uint2 *beta = reinterpret_cast<uint2 *>(bufB + Cn);  // [0,16) fwd, [16,32) inv
+    const u32 p = P.cs.p;
+    const long long R = 1ll << KR;
+    const long long rows = P.nrows * P.chunk;  // truncated: only rows < nrows
+    // staging of the next row pair (PPC == 1): [a row][b row][mbarrier]; the first
+    // pair is requested before the stage table is read
+    constexpr bool STG = RC::STAGE;  // both twist paths (row-major items with tables, else product-major)
+    u32 *stA = reinterpret_cast<u32 *>(tm_s + RC::TABW) + RC::PPC * (2 * Cn + 64);
+    u32 *stB = stA + Cn;
+    uint64_t *mbar = reinterpret_cast<uint64_t *>(stB + Cn);
+    auto stage = [&](long long g) {  // thread 0: bulk copies of work item g's rows
+        const long long np = TT ? g % P.chunk : g / P.nrows;
+        const long long nr = TT ? g / P.chunk : g % P.nrows;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(mbar, 8u * Cn);
+        bulk_g2s(stA, P.Ah + np * (R << KC) + (nr << KC), 4u * Cn, mbar);
+        bulk_g2s(stB, P.Bh + np * (R << KC) + (nr << KC), 4u * Cn, mbar);
+    };
 #if MC_ROW_TM
-    {
+    if constexpr (STG) {
+        // one round trip for the prologue: the merged stage table and the first
+        // row pair land on the mbarrier's first phase (the grid never exceeds
+        // the work items, so every CTA owns one)
+        if (threadIdx.x == 0) {
+            mbar_init(mbar, 1);
+            fence_mbar_init();
+            const long long g = blockIdx.x;
+            const long long np = TT ? g % P.chunk : g / P.nrows;
+            const long long nr = TT ? g / P.chunk : g % P.nrows;
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(mbar, 8u * Cn + 8u * RC::TM);
+            bulk_g2s(stA, P.Ah + np * (R << KC) + (nr << KC), 4u * Cn, mbar);
+            bulk_g2s(stB, P.Bh + np * (R << KC) + (nr << KC), 4u * Cn, mbar);
+            bulk_g2s(tm_s, P.row_tm, 8u * RC::TM, mbar);
+        }
+    } else {
         const uint4 *gm = reinterpret_cast<const uint4 *>(P.row_tm);
         for (int i = threadIdx.x; i < RC::TM / 2; i += RC::THREADS)
             reinterpret_cast<uint4 *>(tm_s)[i] = __ldg(gm + i);
     }
     const TwM W{tm_s};
 #else
+    if (STG && threadIdx.x == 0) {
+        mbar_init(mbar, 1);
+        fence_mbar_init();
+        if ((long long)blockIdx.x < rows) stage(blockIdx.x);
+    }
     {
         const uint4 *gf = reinterpret_cast<const uint4 *>(P.row_tf);
         const uint4 *gi = reinterpret_cast<const uint4 *>(P.row_ti);
@@ -84,26 +122,6 @@ row_conv_kernel(const FourParams P, int KR) {
     }
     const Tw W{tm_s, tm_s + Cn};
 #endif
-    const u32 p = P.cs.p;
-    const long long R = 1ll << KR;
-    const long long rows = P.nrows * P.chunk;  // truncated: only rows < nrows
-    // staging of the next row pair (TT path, PPC == 1): [a row][b row][mbarrier]
-    constexpr bool STG = TT && RC::STAGE;
-    u32 *stA = reinterpret_cast<u32 *>(tm_s + RC::TABW) + RC::PPC * (2 * Cn + 64);
-    u32 *stB = stA + Cn;
-    uint64_t *mbar = reinterpret_cast<uint64_t *>(stB + Cn);
-    auto stage = [&](long long g) {  // thread 0: bulk copies of work item g's rows
-        const long long np = g % P.chunk, nr = g / P.chunk;
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(mbar, 8u * Cn);
-        bulk_g2s(stA, P.Ah + np * (R << KC) + (nr << KC), 4u * Cn, mbar);
-        bulk_g2s(stB, P.Bh + np * (R << KC) + (nr << KC), 4u * Cn, mbar);
-    };
-    if (STG && threadIdx.x == 0) {
-        mbar_init(mbar, 1);
-        fence_mbar_init();
-        if ((long long)blockIdx.x < rows) stage(blockIdx.x);
-    }
     uint32_t phase = 0;
     mc_sync();
 
@@ -197,12 +215,27 @@ row_conv_kernel(const FourParams P, int KR) {
         mc_sync();
 
         u32 va[16], vb[16];
+        if constexpr (STG) {  // the row pair landed in the staging area
+            mbar_wait(mbar, phase);
+            phase ^= 1;
 #pragma unroll
-        for (int s = 0; s < 16; ++s) {
-            const int x = t + G * s;
-            const uint2 bt = beta[s];
-            va[s] = mul_t<AR>(mul_t<AR>(valid ? rowA[x] : 0u, af, afp, p), bt.x, bt.y, p);
-            vb[s] = mul_t<AR>(mul_t<AR>(valid ? rowB[x] : 0u, af, afp, p), bt.x, bt.y, p);
+            for (int s = 0; s < 16; ++s) {
+                const int x = t + G * s;
+                const uint2 bt = beta[s];
+                va[s] = mul_t<AR>(mul_t<AR>(stA[x], af, afp, p), bt.x, bt.y, p);
+                vb[s] = mul_t<AR>(mul_t<AR>(stB[x], af, afp, p), bt.x, bt.y, p);
+            }
+            mc_sync();  // staging consumed: bring in the next work item's rows
+            const long long ng = base + (long long)gridDim.x;
+            if (threadIdx.x == 0 && ng < rows) stage(ng);
+        } else {
+#pragma unroll
+            for (int s = 0; s < 16; ++s) {
+                const int x = t + G * s;
+                const uint2 bt = beta[s];
+                va[s] = mul_t<AR>(mul_t<AR>(valid ? rowA[x] : 0u, af, afp, p), bt.x, bt.y, p);
+                vb[s] = mul_t<AR>(mul_t<AR>(valid ? rowB[x] : 0u, af, afp, p), bt.x, bt.y, p);
+            }
         }
         fwd_top<KC, 16, AR>(va, Cn, t, P.cs, W);
         fwd_top<KC, 16, AR>(vb, Cn, t, P.cs, W);
