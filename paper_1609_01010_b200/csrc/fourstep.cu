@@ -537,7 +537,8 @@ mc_status fourstep_plan(int engine, const u32 *a, long long lda, int z1, const u
     // reads every row once from DRAM, and forming the twists from the small
     // power tables is faster there (config 5, one product per prime: 123.8 ->
     // 121.2 us; config 4, 8 products: 1.063 ms with the tables, 1.166 without)
-    if (twist_table_on(K) && batch >= 2 &&
+    static const bool tw_single = [] { const char *e = getenv("MC_TWIST_SINGLE"); return e && *e; }();
+    if (twist_table_on(K) && (batch >= 2 || tw_single) &&
         (s = get_full_twist(TL, P.tw, KC, &P.twf, &P.twi)) != MC_OK)
         return s;
     P.cs.p = p;

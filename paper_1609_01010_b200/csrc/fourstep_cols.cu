@@ -180,18 +180,10 @@ col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
     u32 *buf0 = reinterpret_cast<u32 *>(tf_s + 2 * C::R);
     u32 *buf1 = buf0 + C::TILE;
     uint64_t *bar = reinterpret_cast<uint64_t *>(buf1 + C::TILE);
-    for (int i = threadIdx.x; i < C::R / 2; i += THREADS)
-        reinterpret_cast<uint4 *>(tf_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_tf) + i);
     const Tw W{tf_s, tf_s};
     const int c = CW * (threadIdx.x % (C::TC / CW));
     const int t = threadIdx.x / (C::TC / CW);
     const u32 p = P.cs.p;
-    if (threadIdx.x == 0) {
-        mbar_init(bar, 1);
-        mbar_init(bar + 1, 1);
-        fence_mbar_init();
-    }
-    mc_sync();
     auto issue = [&](int tile, int k) {  // thread 0
         const int ct = tile % CT, op = (tile / CT) & 1, pc = tile / (2 * CT);
         u32 *dst = k ? buf1 : buf0;
@@ -202,7 +194,16 @@ col_fwd_tma_kernel(const FourParams P, const __grid_constant__ CUtensorMap ta,
             tma_load_3d(dst + bx * BR * C::TC, op ? (const void *)&tb : (const void *)&ta,
                         ct * C::TC, bx * BR, (int)(P.prod0 + pc), bar + k);
     };
-    if (threadIdx.x == 0 && (int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    // the first tile is requested before the stage table is read
+    if (threadIdx.x == 0) {
+        mbar_init(bar, 1);
+        mbar_init(bar + 1, 1);
+        fence_mbar_init();
+        if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    }
+    for (int i = threadIdx.x; i < C::R / 2; i += THREADS)
+        reinterpret_cast<uint4 *>(tf_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_tf) + i);
+    mc_sync();
     uint32_t ph0 = 0, ph1 = 0;
     int k = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -293,12 +294,6 @@ col_inv_async_kernel(const FourParams P, int ntiles) {
     uint2 *tf_s = reinterpret_cast<uint2 *>(smem_raw);
     uint2 *ti_s = tf_s + C::R;
     u32 *bufs = reinterpret_cast<u32 *>(tf_s + 2 * C::R);
-    for (int i = threadIdx.x; i < C::R / 2; i += THREADS) {
-        reinterpret_cast<uint4 *>(ti_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_ti) + i);
-        if (NT < 16)
-            reinterpret_cast<uint4 *>(tf_s)[i] =
-                __ldg(reinterpret_cast<const uint4 *>(P.col_tf) + i);
-    }
     const Tw W{tf_s, ti_s};
     const int c = CW * (threadIdx.x % (C::TC / CW));
     const int t = threadIdx.x / (C::TC / CW);
@@ -315,6 +310,14 @@ col_inv_async_kernel(const FourParams P, int ntiles) {
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0);
+    // stage tables after the first tile's copies are in flight (the loop's first
+    // barrier orders them before the transforms)
+    for (int i = threadIdx.x; i < C::R / 2; i += THREADS) {
+        reinterpret_cast<uint4 *>(ti_s)[i] = __ldg(reinterpret_cast<const uint4 *>(P.col_ti) + i);
+        if (NT < 16)
+            reinterpret_cast<uint4 *>(tf_s)[i] =
+                __ldg(reinterpret_cast<const uint4 *>(P.col_tf) + i);
+    }
     int k = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int ct = tile % CT, pc = tile / CT;

@@ -86,11 +86,6 @@ col_inv3_crt_kernel(const Inv3Params Q, int ntiles) {
     extern __shared__ __align__(1024) uint4 smem_raw[];
     uint2 *ti_s = reinterpret_cast<uint2 *>(smem_raw);
     u32 *bufs = reinterpret_cast<u32 *>(ti_s + 3 * C::R);
-#pragma unroll
-    for (int k = 0; k < 3; ++k)
-        for (int i = threadIdx.x; i < C::R / 2; i += C::THREADS)
-            reinterpret_cast<uint4 *>(ti_s + k * C::R)[i] =
-                __ldg(reinterpret_cast<const uint4 *>(Q.ti[k]) + i);
     const int c = threadIdx.x % C::TC;
     const int t = threadIdx.x / C::TC;
     auto issue = [&](int tile, int k, int sel) {  // every thread: its share of the chunks
@@ -112,6 +107,13 @@ col_inv3_crt_kernel(const Inv3Params Q, int ntiles) {
         mc_sync();
     };
     if ((int)blockIdx.x < ntiles) issue(blockIdx.x, 0, 0);
+    // stage tables after the first copies are in flight (land()'s barrier orders
+    // them before the first transform)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+        for (int i = threadIdx.x; i < C::R / 2; i += C::THREADS)
+            reinterpret_cast<uint4 *>(ti_s + k * C::R)[i] =
+                __ldg(reinterpret_cast<const uint4 *>(Q.ti[k]) + i);
     int sel = 0;  // three steps per tile over two buffers: the parity alternates
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         u32 r1[16], y2[16], v[16];
