@@ -41,14 +41,16 @@ for c, name in names.items():
                      "step, median of the steps; scripts/step_traffic.py)",
            "note": "ncu flushes the caches before each launch: product bytes still dirty in L2 "
                    "when a kernel ends are not counted as writes"}
-    full = {2: "prof_cfg2_summary.txt", 4: "prof_cfg4_row_conv_summary.txt"}.get(c)
+    full = {2: "prof_cfg2_summary.txt", 3: "prof_cfg3_summary.txt", 4: "prof_cfg4_row_conv_summary.txt",
+            5: "prof_cfg5_row_conv_summary.txt"}.get(c)
     if full:
         s = summary(os.path.join(d, full))
         rec["ncu_pipes"] = {
             "fmaheavy_cycles_pct_of_peak": round(float(s["sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed"]), 1),
             "alu_cycles_pct_of_peak": round(float(s["sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active"]), 1),
             "issue_active_pct": round(float(s["smsp__issue_active.avg.pct_of_peak_sustained_active"]), 1),
-            "source": os.path.join(d, full) + (" (row pass: half of the step)" if c == 4 else "")}
+            "source": os.path.join(d, full) + (" (row pass: half of the step)" if c == 4 else
+                                                 " (one prime's row pass, the largest share of the step)" if c == 5 else "")}
     t[name] = rec
 with open("profiles/traffic.json", "w") as f:
     json.dump(t, f, indent=1)
