@@ -21,7 +21,8 @@ namespace mc {
 // per SM.  A quarter of the 16K-word tile of the single-prime pass, so that
 // a 128-register budget holds the first two primes' results (r1, y2) of
 // each slot while the third prime's column transform runs.
-#ifndef MC_INV3_TILE  // words per prime of one column tile (A/B: 8192 = 512 threads, 1 CTA/SM)
+#ifndef MC_INV3_TILE  // words per prime of one column tile (A/B: 8192 = 512 threads, 1 CTA/SM;
+                      // 2048 = 128 threads, 4 CTAs/SM: config 5 119 vs 112 us, 16-byte row chunks)
 #define MC_INV3_TILE 4096
 #endif
 
@@ -37,7 +38,8 @@ struct Col3Cfg {
     static constexpr int PADW = TC < 32 ? TC : 8;
     static constexpr int BUFW = TILE + (R / 16) * PADW;
     static constexpr int SMEM = 3 * R * 8 + 2 * BUFW * 4;
-    static constexpr int MINB = THREADS >= 512 ? 1 : 2;  // 128 registers per thread either way
+    // 128 registers per thread either way (A/B: 2048-word tiles = 128 threads, 4 CTAs/SM)
+    static constexpr int MINB = THREADS >= 512 ? 1 : THREADS >= 256 ? 2 : 4;
     __device__ static __forceinline__ int off(int row) { return row * TC + (row >> 4) * PADW; }
 };
 
