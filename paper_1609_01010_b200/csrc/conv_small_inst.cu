@@ -16,7 +16,10 @@ static cudaError_t launch_nt_fl(const ConvSmallParams &P, cudaStream_t st) {
     auto kern = conv_small_kernel<MC_K, NT, AR, FL>;
     // dynamic shared memory: tables + data (+ TMA staging of both rows)
     const int smem = C::SMEM + (P.tma ? 16 + 4 * (P.za16 + P.zb16) : 0);
-    static int attr_smem = 0, per_sm = 0, per_sm_smem = -1;  // benign races: idempotent
+    struct Once { int attr_smem = 0, per_sm = 0, per_sm_smem = 0; };
+    static PerDevice<Once> once;
+    int &attr_smem = once.get().attr_smem, &per_sm = once.get().per_sm,
+        &per_sm_smem = once.get().per_sm_smem;
     if (smem > attr_smem) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              smem);
@@ -95,7 +98,8 @@ static cudaError_t launch_xf(const XformParams &X, cudaStream_t st) {
     using C = SmallCfg<MC_K>;
     auto kern = xform_small_kernel<MC_K, MODE, NT>;
     const int smem = C::L * 8 + C::PPC * C::L * 4;
-    static int per_sm = 0;  // benign race: idempotent
+    static PerDevice<int> per_sm_dev;
+    int &per_sm = per_sm_dev.get();
     if (!per_sm) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;

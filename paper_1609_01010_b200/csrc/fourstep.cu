@@ -403,7 +403,8 @@ mc_status get_twist_tables(u32 p, int K, const u32 **lo_f, const uint2 **hi_f, c
 template <int KC, int AR, bool TT>
 static cudaError_t launch_rows_lz(const FourParams &P, int KR, cudaStream_t st) {
     using RC = RowCfg<KC>;
-    static int per_sm = 0;
+    static PerDevice<int> per_sm_dev;
+    int &per_sm = per_sm_dev.get();
     if (!per_sm) {
         cudaError_t e = prep_kernel(row_conv_kernel<KC, AR, TT>, RC::SMEM, RC::THREADS, &per_sm);
         if (e != cudaSuccess) return e;

@@ -376,7 +376,8 @@ col_inv_async_kernel(const FourParams P, int ntiles) {
 template <int KR, int KC, int NT, int AR, int CW = MC_COL_CW, int TL = MC_COL_TILE>
 static cudaError_t launch_inv_async(const FourParams &P, cudaStream_t st) {
     using C = ColCfg<KR, TL>;
-    static bool ready = false;
+    static PerDevice<bool> ready_dev;
+    bool &ready = ready_dev.get();
     if (!ready) {
         cudaError_t e = prep_kernel(col_inv_async_kernel<KR, KC, NT, AR, CW, TL>,
                                     ColInvAsync<KR, TL>::SMEM, C::THREADS / CW, nullptr);
@@ -401,7 +402,8 @@ template <int KR, int KC, int NT, int AR, int CW = MC_COL_CW, int TL = MC_COL_TI
 static cudaError_t launch_fwd_tma(const FourParams &P, const ColTma &M, cudaStream_t st) {
     using C = ColCfg<KR, TL>;
     constexpr int SMEM = 2 * C::R * 8 + 2 * C::TILE * 4 + 64;
-    static bool ready = false;
+    static PerDevice<bool> ready_dev;
+    bool &ready = ready_dev.get();
     if (!ready) {
         cudaError_t e =
             prep_kernel(col_fwd_tma_kernel<KR, KC, NT, AR, CW, TL>, SMEM, C::THREADS / CW, nullptr);
@@ -433,7 +435,8 @@ static cudaError_t launch_one(const FourParams &P, bool fwd, cudaStream_t st,
         if (!fwd && col_inv_async_on()) return launch_inv_async<KR, KC, NT, AR>(P, st);
     }
     using C = ColCfg<KR>;
-    static bool ready_f = false, ready_i = false;  // benign races: idempotent
+    static PerDevice<bool> ready_f_dev, ready_i_dev;
+    bool &ready_f = ready_f_dev.get(), &ready_i = ready_i_dev.get();
     dim3 grid((unsigned)((1u << KC) / C::TC), fwd ? 2u : 1u, (unsigned)P.chunk);
     if (fwd) {
         if (!ready_f) {

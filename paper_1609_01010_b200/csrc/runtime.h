@@ -74,6 +74,21 @@ constexpr int kMaxStageTableLog2 = 16;
 mc_status get_tables(u32 p, int log2L, const FieldTables **out);
 
 int current_device();
+// Launch-time state that belongs to one device: kernel attributes
+// (cudaFuncSetAttribute) and occupancy figures live in the device's context,
+// so a process that drives several GPUs needs them once per device.
+// `static PerDevice<T> x;` at the launch site, `x.get()` = the slot of the
+// calling thread's current device.  Races between threads are benign: every
+// writer stores the same value after the same idempotent runtime calls.
+constexpr int kMaxDevices = 64;
+template <class T>
+struct PerDevice {
+    T v[kMaxDevices] = {};
+    T &get() {
+        const int d = current_device();
+        return v[d >= 0 && d < kMaxDevices ? d : 0];
+    }
+};
 void keep_pool_memory();
 // Lazy-range arithmetic (modarith.cuh) is valid for p < 2^30; MC_NO_LAZY
 // (non-empty) forces the canonical kernels for A/B runs.

@@ -159,7 +159,8 @@ col_inv3_crt_kernel(const Inv3Params Q, int ntiles) {
 template <int KR, int AR0, int AR1>
 static cudaError_t launch_inv3(const Inv3Params &Q, cudaStream_t st) {
     using C = Col3Cfg<KR>;
-    static bool ready = false;
+    static PerDevice<bool> ready_dev;
+    bool &ready = ready_dev.get();
     if (!ready) {
         cudaError_t e = prep_kernel(col_inv3_crt_kernel<KR, 12, AR0, AR1>, C::SMEM, C::THREADS,
                                     nullptr);

@@ -533,12 +533,13 @@ static mc_status rows_launch(int mode, const u32 *x, long long ldx, int z, u32 *
     const int L = 1 << K;
     const int threads = std::max(32, std::min(512, L / 16));
     const size_t smem = 4ull * (L + L / 16 + 1);
-    static const int max_dyn = [] {
-        cudaFuncSetAttribute(rows_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * ((1 << kRowsMaxK) + (1 << (kRowsMaxK - 4)) + 1));
-        cudaFuncSetAttribute(rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * ((1 << kRowsMaxK) + (1 << (kRowsMaxK - 4)) + 1));
-        return 4 * ((1 << kRowsMaxK) + (1 << (kRowsMaxK - 4)) + 1);
-    }();
-    (void)max_dyn;
+    static PerDevice<bool> attr_dev;
+    if (bool &attr = attr_dev.get(); !attr) {
+        constexpr int max_dyn = 4 * ((1 << kRowsMaxK) + (1 << (kRowsMaxK - 4)) + 1);
+        MC_CUDA_CHECK(cudaFuncSetAttribute(rows_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
+        MC_CUDA_CHECK(cudaFuncSetAttribute(rows_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, max_dyn));
+        attr = true;
+    }
     const int per_sm = std::max(1, std::min(2048 / threads, (int)((200u << 10) / smem)));
     const long long grid = std::min<long long>(batch, (long long)sm_count() * per_sm);
     if (mode == 0)
